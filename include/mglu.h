@@ -1,0 +1,164 @@
+/*
+ * mglu.h -- C ABI of libmglu: the FlashMGLU forward pass (MoEG / SwiMGLU up-projection) on
+ * B200 (sm_100a).
+ *
+ * What it computes (Eq. 3, "MoEG Variant"):
+ *
+ *     y = sum_{i=1..n_m} g( x (M_i (.) W) ) (.) ( x (Mbar_i (.) W) ),   Mbar_i = 1 - M_i
+ *
+ * for every token row of x, with one shared weight W and n_m binary masks M_i that are fixed at
+ * inference ("At inference, all masks are fixed, and the fused masked projections execute with
+ * a single kernel").  The kernels read W and the packed masks from HBM once per call
+ * (P:245), accumulate the unmasked product t and the gated sums s_i in one pass
+ * (Alg. 1), form the value stream as t - s_i and apply g, the product
+ * and the sum over i on chip.
+ *
+ * Letters (reading R2, BASELINE naming): d = reduction (model) dim, h = output
+ * (intermediate) dim, B = tokens.
+ *
+ * ---------------------------------------------------------------------------------------------
+ * Layouts (all row-major, contiguous, no padding):
+ *   x        [B][d]   dtype of the handle (bf16 or f32)
+ *   Wt       [h][d]   dtype of the handle.  Row j is column j of the logical W (d x h), i.e.
+ *                     Alg. 1's A and nn.Linear.weight.
+ *   packed   h*d*n_m/8 bytes: the dense code layout (reading R3).  Element (j,k)'s
+ *                     n_m-bit code c[j,k] occupies stream bits [n_m*(j*d+k), n_m*(j*d+k)+n_m);
+ *                     stream bit q is bit (q mod 8) of byte q/8 (little-endian).  Mask M_i is bit
+ *                     (i-1) of the code (Alg. 1: "mask[row,k] AND (1 << (i-1))").
+ *                     Rows of Wt own contiguous byte ranges [j*d*n_m/8, (j+1)*d*n_m/8), so an
+ *                     h-shard of a layer is a pointer offset into Wt and into packed.
+ *   out      [B][h]   dtype of the handle; bf16 stored round-to-nearest-even from fp32.
+ *   z        [B][2*n_m][h] fp32 (debug partials, Alg. 1's accumulator order P:208):
+ *                     z[b][i-1][j] = gate_i = s_i,   z[b][n_m+i-1][j] = value_i = t - s_i.
+ *
+ * Ownership: every data pointer is BORROWED.  The caller allocates x, Wt, packed, out, z (device
+ * memory unless the entry point says "host") and keeps them alive until the work queued on
+ * `stream` has completed.  A handle owns only its configuration, a TMA-descriptor cache and a
+ * small device workspace allocated at create time; mglu_forward never allocates, never frees and
+ * never synchronises (it enqueues kernels on `stream` and returns).
+ *
+ * Errors: every call returns mglu_status; nothing throws or aborts across the ABI.  Argument
+ * errors are detected before any launch.  Launch failures return MGLU_ERR_CUDA with the CUDA
+ * error string available from mglu_last_error(handle).  Faults inside a kernel surface at the
+ * caller's next synchronisation, as in CUDA.
+ *
+ * Threading: a handle is immutable after mglu_create except for mglu_set_path and its internal
+ * caches (guarded by a mutex); concurrent mglu_forward calls on different streams are allowed.
+ * Streams are `cudaStream_t` passed as void* (NULL = the legacy default stream).
+ */
+#ifndef MGLU_H_
+#define MGLU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mglu_ctx* mglu_handle;
+
+typedef enum {
+  MGLU_OK = 0,
+  MGLU_ERR_INVALID_ARG = 1,   /* null pointer, negative size, bad enum, dtype mismatch       */
+  MGLU_ERR_UNSUPPORTED = 2,   /* n_m not in {1,2,4,8}; d % 8 != 0; path not available for cfg */
+  MGLU_ERR_MISALIGNED = 3,    /* a data pointer not 16-byte aligned                           */
+  MGLU_ERR_CUDA = 4,          /* a CUDA runtime/driver call failed; see mglu_last_error()     */
+  MGLU_ERR_OOM = 5            /* workspace allocation failed                                  */
+} mglu_status;
+
+/* g of Eq. 1/3 (reading R5): Swish = z*sigmoid(z) (SiLU, beta = 1); GELU exact erf form. */
+typedef enum {
+  MGLU_ACT_IDENTITY = 0,
+  MGLU_ACT_SWISH = 1,
+  MGLU_ACT_GELU = 2,
+  MGLU_ACT_RELU = 3,
+  MGLU_ACT_SIGMOID = 4
+} mglu_activation;
+
+typedef enum { MGLU_BF16 = 0, MGLU_F32 = 1 } mglu_dtype;
+
+/* Kernel regime.  AUTO picks by dtype and B.  The others force one
+ * kernel (for tests and benchmarks); forcing a path that cannot serve the configuration makes
+ * mglu_forward return MGLU_ERR_UNSUPPORTED. */
+typedef enum {
+  MGLU_PATH_AUTO = 0,
+  MGLU_PATH_SIMT = 1,     /* CUDA-core fused masked GEMV (Alg. 1 without split-K), any dtype/B   */
+  MGLU_PATH_MMA = 2,      /* register-masked mma.sync GEMV, bf16, streams W+codes once per 8 tok */
+  MGLU_PATH_TCGEN05 = 3   /* tcgen05/TMEM masked GEMM, bf16, prefill / large B                  */
+} mglu_path;
+
+/* Create a handle for one (d, h, n_m, act, dtype) layer on CUDA device `device`.
+ *   d, h >= 1; d % 8 == 0 (8 elements = n_m whole bytes of codes, 16-byte row alignment);
+ *   n_m in {1, 2, 4, 8} (dense byte-aligned code widths, reading R3).
+ * Errors: INVALID_ARG (null out, bad enum, d/h < 1), UNSUPPORTED (n_m, d % 8), CUDA, OOM. */
+mglu_status mglu_create(mglu_handle* out, int64_t d, int64_t h, int n_m, int act, int dtype,
+                        int device);
+
+/* Destroy a handle (frees its workspace).  NULL is a no-op returning MGLU_OK. */
+mglu_status mglu_destroy(mglu_handle hd);
+
+/* Force a kernel regime (mglu_path).  INVALID_ARG for an unknown value. */
+mglu_status mglu_set_path(mglu_handle hd, int path);
+
+/* The forward pass: out[B][h] = Eq. 3 of x[B][d] (device pointers, 16-byte aligned).
+ * B == 0 is a valid empty call (returns MGLU_OK, launches nothing).
+ * Errors: INVALID_ARG (null pointer, B < 0), MISALIGNED, UNSUPPORTED (forced path cannot serve
+ * this B/dtype), CUDA. */
+mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* Wt,
+                         const void* packed, void* out, void* stream);
+
+/* Debug/test: Alg. 1's accumulators z[B][2*n_m][h] fp32 (see Layouts) instead of y.  Same
+ * single pass over W and the codes; runs the SIMT regime.  Errors as mglu_forward. */
+mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, const void* Wt,
+                                  const void* packed, float* z, void* stream);
+
+/* End-to-end form: x_host [B][d] and out_host [B][h] are HOST buffers (pinned for async
+ * copies; pageable works but serialises).  Copies x to the handle's device staging buffer,
+ * runs mglu_forward, copies y back, all enqueued on `stream` (the caller synchronises).  The
+ * staging buffer is allocated at the first call for a given B and reused (grown, never shrunk).
+ * Errors as mglu_forward plus OOM. */
+mglu_status mglu_forward_host(mglu_handle hd, const void* x_host, int64_t B, const void* Wt,
+                              const void* packed, void* out_host, void* stream);
+
+/* Number of packed-code bytes of an (h x d) layer with n_m masks: ceil(h*d*n_m/8) (Table 1's
+ * n_m*hd mask bits).  Returns 0 for invalid arguments. */
+size_t mglu_packed_mask_bytes(int64_t d, int64_t h, int n_m);
+
+/* Offline mask packing ("all masks are fixed"; "Combine the n_m binary masks ...").
+ *   bits   [n_m][h][d] uint8, each 0 or 1 (INVALID_ARG on any other value)
+ *   logits [n_m][h][d] float32; bit = (logit > 0), strict (Alg. 2; reading R4)
+ *   packed mglu_packed_mask_bytes(d, h, n_m) bytes (written entirely)
+ * Host variants work on host memory, run synchronously and validate every bit byte; device
+ * variants take device pointers, enqueue one kernel on `stream` and use bit (b & 1) of each byte
+ * (a device-side value check could only be reported after a synchronisation). */
+mglu_status mglu_pack_masks_host(const uint8_t* bits, int n_m, int64_t h, int64_t d,
+                                 uint8_t* packed);
+mglu_status mglu_pack_logits_host(const float* logits, int n_m, int64_t h, int64_t d,
+                                  uint8_t* packed);
+mglu_status mglu_unpack_masks_host(const uint8_t* packed, int n_m, int64_t h, int64_t d,
+                                   uint8_t* bits);
+mglu_status mglu_pack_masks_device(const uint8_t* bits, int n_m, int64_t h, int64_t d,
+                                   uint8_t* packed, void* stream);
+mglu_status mglu_pack_logits_device(const float* logits, int n_m, int64_t h, int64_t d,
+                                    uint8_t* packed, void* stream);
+mglu_status mglu_unpack_masks_device(const uint8_t* packed, int n_m, int64_t h, int64_t d,
+                                     uint8_t* bits, void* stream);
+
+/* Number of kernels the last mglu_forward on this handle enqueued (for launch accounting). */
+int mglu_last_launch_count(mglu_handle hd);
+
+/* Which mglu_path the last mglu_forward on this handle ran. */
+int mglu_last_path(mglu_handle hd);
+
+/* Static strings; never NULL. */
+const char* mglu_status_string(mglu_status s);
+const char* mglu_last_error(mglu_handle hd);
+
+/* Library version, "major.minor.patch". */
+const char* mglu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGLU_H_ */

@@ -1,0 +1,272 @@
+"""Thin Python binding of libmglu (include/mglu.h) -- argument marshalling only.
+
+Every step of the forward pass runs in the CUDA kernels of ``libmglu.so``; this module converts
+torch tensors / numpy arrays to raw pointers, picks torch's current stream and turns status codes
+into exceptions.  There is no CPU fallback: if the library is missing, importing the binding
+raises :class:`MgluLibraryMissing`.
+
+The functions carry the C names (``mglu_create``, ``mglu_forward``, ...); :class:`Mglu` is a
+small convenience wrapper owning a handle.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import torch
+
+_PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG_DIR, "libmglu.so")
+HEADER_PATH = os.path.join(os.path.dirname(_PKG_DIR), "include", "mglu.h")
+
+MGLU_OK, MGLU_ERR_INVALID_ARG, MGLU_ERR_UNSUPPORTED, MGLU_ERR_MISALIGNED, MGLU_ERR_CUDA, MGLU_ERR_OOM = range(6)
+ACT = {"identity": 0, "swish": 1, "gelu": 2, "relu": 3, "sigmoid": 4}
+DTYPE = {"bf16": 0, "f32": 1}
+PATH = {"auto": 0, "simt": 1, "mma": 2, "tcgen05": 3}
+TORCH_DTYPE = {"bf16": torch.bfloat16, "f32": torch.float32}
+
+
+class MgluLibraryMissing(ImportError):
+    pass
+
+
+class MgluError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libmglu.so (built in-tree by ``paper_2506_23225_b200.build``)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise MgluLibraryMissing(
+            f"{path} not found: build it with `python -m paper_2506_23225_b200.build` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    vp, i64, c_int, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+    u8p = ctypes.POINTER(ctypes.c_uint8)
+    f32p = ctypes.POINTER(ctypes.c_float)
+    sig = {
+        "mglu_create": ([ctypes.POINTER(vp), i64, i64, c_int, c_int, c_int, c_int], c_int),
+        "mglu_destroy": ([vp], c_int),
+        "mglu_set_path": ([vp, c_int], c_int),
+        "mglu_forward": ([vp, vp, i64, vp, vp, vp, vp], c_int),
+        "mglu_forward_partials": ([vp, vp, i64, vp, vp, vp, vp], c_int),
+        "mglu_forward_host": ([vp, vp, i64, vp, vp, vp, vp], c_int),
+        "mglu_packed_mask_bytes": ([i64, i64, c_int], sz),
+        "mglu_pack_masks_host": ([vp, c_int, i64, i64, vp], c_int),
+        "mglu_pack_logits_host": ([vp, c_int, i64, i64, vp], c_int),
+        "mglu_unpack_masks_host": ([vp, c_int, i64, i64, vp], c_int),
+        "mglu_pack_masks_device": ([vp, c_int, i64, i64, vp, vp], c_int),
+        "mglu_pack_logits_device": ([vp, c_int, i64, i64, vp, vp], c_int),
+        "mglu_unpack_masks_device": ([vp, c_int, i64, i64, vp, vp], c_int),
+        "mglu_last_launch_count": ([vp], c_int),
+        "mglu_last_path": ([vp], c_int),
+        "mglu_status_string": ([c_int], ctypes.c_char_p),
+        "mglu_last_error": ([vp], ctypes.c_char_p),
+        "mglu_version": ([], ctypes.c_char_p),
+    }
+    del u8p, f32p
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def header_functions(path: str = HEADER_PATH) -> list[str]:
+    """Names of every function declared in include/mglu.h."""
+    text = open(path).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mglu_[a-z_0-9]+)\s*\(", text)))
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    raise TypeError(type(t))
+
+
+def _stream_ptr(stream, device) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return stream.cuda_stream if isinstance(stream, torch.cuda.Stream) else int(stream)
+
+
+def status_string(status: int) -> str:
+    return load_library().mglu_status_string(status).decode()
+
+
+def _check(status: int, handle=None, what: str = ""):
+    if status != MGLU_OK:
+        lib = load_library()
+        detail = lib.mglu_last_error(handle).decode() if handle else ""
+        raise MgluError(status, f"{what}: {status_string(status)} {detail}".strip())
+
+
+# ------------------------------------------------------------------ C-named entry points
+def mglu_create(d: int, h: int, n_m: int, act: int, dtype: int, device: int) -> int:
+    lib = load_library()
+    hd = ctypes.c_void_p()
+    _check(lib.mglu_create(ctypes.byref(hd), d, h, n_m, act, dtype, device), None, "mglu_create")
+    return hd.value
+
+
+def mglu_destroy(handle: int) -> None:
+    _check(load_library().mglu_destroy(handle), None, "mglu_destroy")
+
+
+def mglu_set_path(handle: int, path: int) -> None:
+    _check(load_library().mglu_set_path(handle, path), handle, "mglu_set_path")
+
+
+def mglu_forward(handle, x, B, Wt, packed, out, stream=None) -> None:
+    _check(load_library().mglu_forward(handle, _ptr(x), B, _ptr(Wt), _ptr(packed), _ptr(out),
+                                       _stream_ptr(stream, x.device)), handle, "mglu_forward")
+
+
+def mglu_forward_partials(handle, x, B, Wt, packed, z, stream=None) -> None:
+    _check(load_library().mglu_forward_partials(handle, _ptr(x), B, _ptr(Wt), _ptr(packed), _ptr(z),
+                                                _stream_ptr(stream, Wt.device)),
+           handle, "mglu_forward_partials")
+
+
+def mglu_forward_host(handle, x_host, B, Wt, packed, out_host, stream=None) -> None:
+    _check(load_library().mglu_forward_host(handle, _ptr(x_host), B, _ptr(Wt), _ptr(packed),
+                                            _ptr(out_host), _stream_ptr(stream, Wt.device)),
+           handle, "mglu_forward_host")
+
+
+def mglu_packed_mask_bytes(d: int, h: int, n_m: int) -> int:
+    return int(load_library().mglu_packed_mask_bytes(d, h, n_m))
+
+
+def mglu_pack_masks_host(bits: np.ndarray) -> np.ndarray:
+    bits = np.ascontiguousarray(bits, dtype=np.uint8)
+    n_m, h, d = bits.shape
+    out = np.empty(mglu_packed_mask_bytes(d, h, n_m), dtype=np.uint8)
+    _check(load_library().mglu_pack_masks_host(_ptr(bits), n_m, h, d, _ptr(out)), None, "pack_masks_host")
+    return out
+
+
+def mglu_pack_logits_host(logits: np.ndarray) -> np.ndarray:
+    logits = np.ascontiguousarray(logits, dtype=np.float32)
+    n_m, h, d = logits.shape
+    out = np.empty(mglu_packed_mask_bytes(d, h, n_m), dtype=np.uint8)
+    _check(load_library().mglu_pack_logits_host(_ptr(logits), n_m, h, d, _ptr(out)), None, "pack_logits_host")
+    return out
+
+
+def mglu_unpack_masks_host(packed: np.ndarray, n_m: int, h: int, d: int) -> np.ndarray:
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    out = np.empty((n_m, h, d), dtype=np.uint8)
+    _check(load_library().mglu_unpack_masks_host(_ptr(packed), n_m, h, d, _ptr(out)), None, "unpack_masks_host")
+    return out
+
+
+def mglu_pack_masks_device(bits: torch.Tensor, stream=None) -> torch.Tensor:
+    assert bits.is_cuda and bits.dtype == torch.uint8 and bits.is_contiguous()
+    n_m, h, d = bits.shape
+    out = torch.empty(mglu_packed_mask_bytes(d, h, n_m), dtype=torch.uint8, device=bits.device)
+    _check(load_library().mglu_pack_masks_device(_ptr(bits), n_m, h, d, _ptr(out),
+                                                 _stream_ptr(stream, bits.device)), None, "pack_masks_device")
+    return out
+
+
+def mglu_pack_logits_device(logits: torch.Tensor, stream=None) -> torch.Tensor:
+    assert logits.is_cuda and logits.dtype == torch.float32 and logits.is_contiguous()
+    n_m, h, d = logits.shape
+    out = torch.empty(mglu_packed_mask_bytes(d, h, n_m), dtype=torch.uint8, device=logits.device)
+    _check(load_library().mglu_pack_logits_device(_ptr(logits), n_m, h, d, _ptr(out),
+                                                  _stream_ptr(stream, logits.device)), None, "pack_logits_device")
+    return out
+
+
+def mglu_unpack_masks_device(packed: torch.Tensor, n_m: int, h: int, d: int, stream=None) -> torch.Tensor:
+    assert packed.is_cuda and packed.dtype == torch.uint8
+    out = torch.empty((n_m, h, d), dtype=torch.uint8, device=packed.device)
+    _check(load_library().mglu_unpack_masks_device(_ptr(packed), n_m, h, d, _ptr(out),
+                                                   _stream_ptr(stream, packed.device)), None, "unpack_masks_device")
+    return out
+
+
+# ------------------------------------------------------------------ convenience wrapper
+class Mglu:
+    """One MGLU up-projection layer configuration (d, h, n_m, activation, dtype) on a device.
+    Weights and packed codes are passed per call (borrowed, as in the C ABI)."""
+
+    def __init__(self, d: int, h: int, n_m: int, act: str = "swish", dtype: str = "bf16",
+                 device: int = 0, path: str = "auto"):
+        self.d, self.h, self.n_m, self.act, self.dtype, self.device = d, h, n_m, act, dtype, device
+        self.handle = mglu_create(d, h, n_m, ACT[act], DTYPE[dtype], device)
+        if path != "auto":
+            self.set_path(path)
+
+    def set_path(self, path: str) -> None:
+        mglu_set_path(self.handle, PATH[path])
+
+    def _check_inputs(self, x, Wt, packed):
+        td = TORCH_DTYPE[self.dtype]
+        if x.dtype != td or Wt.dtype != td:
+            raise MgluError(MGLU_ERR_INVALID_ARG, f"x/Wt must be {td}")
+        if tuple(Wt.shape) != (self.h, self.d) or x.shape[-1] != self.d:
+            raise MgluError(MGLU_ERR_INVALID_ARG, "shape mismatch")
+        if packed.dtype != torch.uint8 or packed.numel() != mglu_packed_mask_bytes(self.d, self.h, self.n_m):
+            raise MgluError(MGLU_ERR_INVALID_ARG, "packed codes size mismatch")
+        if not (x.is_contiguous() and Wt.is_contiguous() and packed.is_contiguous()):
+            raise MgluError(MGLU_ERR_INVALID_ARG, "tensors must be contiguous")
+
+    def forward(self, x: torch.Tensor, Wt: torch.Tensor, packed: torch.Tensor,
+                out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        self._check_inputs(x, Wt, packed)
+        B = x.shape[0] if x.dim() == 2 else 1
+        if out is None:
+            out = torch.empty((B, self.h), dtype=TORCH_DTYPE[self.dtype], device=x.device)
+        mglu_forward(self.handle, x, B, Wt, packed, out, stream)
+        return out
+
+    __call__ = forward
+
+    def forward_partials(self, x, Wt, packed, stream=None) -> torch.Tensor:
+        self._check_inputs(x, Wt, packed)
+        B = x.shape[0]
+        z = torch.empty((B, 2 * self.n_m, self.h), dtype=torch.float32, device=x.device)
+        mglu_forward_partials(self.handle, x, B, Wt, packed, z, stream)
+        return z
+
+    def forward_host(self, x_host: torch.Tensor, Wt: torch.Tensor, packed: torch.Tensor,
+                     out_host: torch.Tensor, stream=None) -> torch.Tensor:
+        B = x_host.shape[0]
+        mglu_forward_host(self.handle, x_host, B, Wt, packed, out_host, stream)
+        return out_host
+
+    def last_path(self) -> str:
+        v = load_library().mglu_last_path(self.handle)
+        return {k: p for p, k in PATH.items()}.get(v, str(v))
+
+    def last_launch_count(self) -> int:
+        return int(load_library().mglu_last_launch_count(self.handle))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            mglu_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
