@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""bench.py -- the FlashMGLU forward pass (SwiMGLU up-projection) on B200.
+
+Default workload (N=1): BASELINE.json's target row -- batch-1 SwiMGLU, n_m = 4, d = 4096,
+h = 14336, bf16 (config 3 at B = 1).  One step = one forward call (all SURVEY 8(a) rows run in
+one kernel).  For N > 1 the layer's output columns (h) are column-sharded across ranks with no
+data-path collective (reading R-e); value = the whole layer's algorithmic bytes / max-over-ranks
+time, "scaling": "strong" (total work fixed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mglu|reference] [--workload NAME]
+
+Timing: W untimed warm-up steps, a ~0.3 s clock window (untimed, nvidia-smi/NVML sampled), then
+EXACTLY K steps between CUDA events on the launching stream, bracketed by barrier + synchronize.
+L2: the per-step inputs are larger than L2 -- L distinct copies of the layer (W + codes,
+L x 147 MB) are rotated, so every step streams cold weights (no flush kernel is needed).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+WORKLOADS = {
+    # name: (d, h, n_m, B, act, description)
+    "decode_b1": (4096, 14336, 4, 1, "swish", "config3 batch-1 SwiMGLU d=4096 h=14336 n_m=4 (Llama-3-8B FFN)"),
+    "decode7b_b1": (4096, 11008, 4, 1, "swish", "config2 batch-1 SwiMGLU d=4096 h=11008 n_m=4 (LLaMA-7B FFN)"),
+    "decode_b8": (4096, 14336, 4, 8, "swish", "config3 batch-8 SwiMGLU d=4096 h=14336 n_m=4"),
+    "sweep_b1_nm1": (8192, 28672, 1, 1, "swish", "config5 batch-1 d=8192 h=28672 n_m=1"),
+    "sweep_b1_nm2": (8192, 28672, 2, 1, "swish", "config5 batch-1 d=8192 h=28672 n_m=2"),
+    "sweep_b1_nm4": (8192, 28672, 4, 1, "swish", "config5 batch-1 d=8192 h=28672 n_m=4"),
+    "sweep_b1_nm8": (8192, 28672, 8, 1, "swish", "config5 batch-1 d=8192 h=28672 n_m=8"),
+}
+DEFAULT_WORKLOAD = "decode_b1"
+METRIC = "SwiMGLU up-proj HBM GB/s at batch 1 (algorithmic W+codes+x+y bytes / time per call)"
+
+
+def algorithmic_bytes(d, h, n_m, B, elem=2):
+    """W once, the packed codes once (n_m bits/element), x read, y written."""
+    return h * d * elem + (h * d * n_m + 7) // 8 + B * d * elem + B * h * elem
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            pk = json.load(f)
+        return {"hbm_gbs": pk["hbm_gbs"], "bf16_tflops": pk["bf16_tflops"],
+                "bf16_tflops_sustained": pk.get("bf16_tflops_sustained"), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------- clocks (NVML)
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+            self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- distributed plumbing
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(ws, value: float) -> float:
+    if ws == 1:
+        return value
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- inputs (synthetic, seeded)
+def make_layers(d, h_local, n_m, B, L, seed, rank):
+    """L distinct copies of the rank's layer shard, drawn on the device (synth recipe: x ~ N(0,1),
+    Wt ~ U(+-1/sqrt(d)), code bits i.i.d. Bernoulli(0.5))."""
+    from synth import random_packed_codes
+    g = torch.Generator(device="cuda").manual_seed(seed * 1000 + rank)
+    x = torch.randn(B, d, device="cuda", generator=g).to(torch.bfloat16)
+    layers = []
+    for li in range(L):
+        Wt = ((torch.rand(h_local, d, device="cuda", generator=g) * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+        codes = random_packed_codes(seed * 7919 + rank * 97 + li, h_local, d, n_m, device="cuda")
+        layers.append((Wt, codes))
+    return x, layers
+
+
+def time_steps(fn_step, K, stream):
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(K):
+        fn_step(k)
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / 1e3   # seconds
+
+
+def cublas_swiglu_us(d, h, B, L, K, stream):
+    """Same-box cuBLAS SwiGLU up-projection at equal d/h/B (bf16): (i) two GEMMs + silu*mul,
+    (ii) one GEMM on the concatenated [2h x d] weight + split + silu*mul.  L rotated weight
+    copies (inputs > L2), CUDA-graph replay of K steps; returns the faster, microseconds/call."""
+    g = torch.Generator(device="cuda").manual_seed(123)
+    x = torch.randn(B, d, device="cuda", generator=g).to(torch.bfloat16)
+    Ws = [(torch.randn(2 * h, d, device="cuda", generator=g) * 0.01).to(torch.bfloat16) for _ in range(L)]
+    res = {}
+    for variant in ("two_gemm", "concat_gemm"):
+        def step(k, Ws=Ws, variant=variant):
+            W = Ws[k % L]
+            if variant == "two_gemm":
+                a = torch.matmul(x, W[:h].t())
+                b = torch.matmul(x, W[h:].t())
+            else:
+                ab = torch.matmul(x, W.t())
+                a, b = ab[:, :h], ab[:, h:]
+            return torch.nn.functional.silu(a) * b
+        with torch.cuda.stream(stream):
+            for k in range(3):
+                step(k)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                for k in range(K):
+                    step(k)
+            graph.replay()
+            stream.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            graph.replay()
+            e1.record(stream)
+            e1.synchronize()
+        res[variant] = e0.elapsed_time(e1) * 1e3 / K
+        del graph
+    res["best_us"] = min(res["two_gemm"], res["concat_gemm"])
+    return res
+
+
+def cpu_baseline(d, h, n_m, B, act_code, budget_s=10.0):
+    """The oracle as it stands (C, binary64, OpenMP over output columns) on the same workload:
+    full layer (all h columns, all d) per pass, passes repeated until ~budget_s of CPU work."""
+    from oracle import COracle
+    o = COracle()
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((B, d))
+    Wt = rng.uniform(-1 / d ** 0.5, 1 / d ** 0.5, (h, d))
+    packed = rng.integers(0, 256, (h * d * n_m + 7) // 8, dtype=np.uint8)
+    cols = np.arange(h)
+    passes, t0 = 0, time.perf_counter()
+    while True:
+        o.forward(x, Wt, cols, packed, n_m, act_code)
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or passes >= 200:
+            break
+    per = el / passes
+    return {"value": algorithmic_bytes(d, h, n_m, B) / per / 1e9, "unit": "GB/s",
+            "cores": o.num_threads(), "kind": "oracle",
+            "sample": f"full layer (B={B}, all {h} columns x {d}), {passes} passes in {el:.1f} s",
+            "seconds_per_call": per}
+
+
+# ---------------------------------------------------------------- arms
+def run_reference(args, ws, rank):
+    """--impl reference: the CPU oracle as it stands, timed on the host cores, on this arm's
+    workload/metric.  Rank 0 only; other ranks exit without work."""
+    if rank != 0:
+        return None
+    from oracle import ACT_NAMES, COracle
+    d, h, n_m, B, act, desc = WORKLOADS[args.workload]
+    o = COracle()
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((B, d))
+    Wt = rng.uniform(-1 / d ** 0.5, 1 / d ** 0.5, (h, d))
+    packed = rng.integers(0, 256, (h * d * n_m + 7) // 8, dtype=np.uint8)
+    cols = np.arange(h)
+    for _ in range(args.warmup):
+        o.forward(x, Wt, cols, packed, n_m, ACT_NAMES[act])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.forward(x, Wt, cols, packed, n_m, ACT_NAMES[act])
+    el = time.perf_counter() - t0
+    per = el / args.steps
+    value = algorithmic_bytes(d, h, n_m, B) * args.steps / el / 1e9
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": desc, "d": d, "h": h, "n_m": n_m, "batch": B, "act": act},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": o.num_threads(), "kind": "oracle",
+                         "sample": f"full layer per step (B={B}, {h} columns x {d})"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def run_mglu(args, ws, rank, local):
+    from paper_2506_23225_b200.build import build
+    if rank == 0:
+        build()
+    barrier(ws)
+    from paper_2506_23225_b200.mglu import Mglu
+    d, h, n_m, B, act, desc = WORKLOADS[args.workload]
+    # column shard of h (no exchange on the hot path)
+    lo, hi = rank * h // ws, (rank + 1) * h // ws
+    h_loc = hi - lo
+    L = args.layers
+    x, layers = make_layers(d, h_loc, n_m, B, L, seed=0, rank=rank)
+    y = torch.empty(B, h_loc, device="cuda", dtype=torch.bfloat16)
+    layer = Mglu(d, h_loc, n_m, act=act, dtype="bf16", device=local, path=args.path)
+    stream = torch.cuda.Stream()
+
+    calls = [layer.bind(x, Wt, codes, y, stream=stream) for Wt, codes in layers]
+
+    def step(k):
+        calls[k % L]()
+
+    with torch.cuda.stream(stream):
+        for k in range(args.warmup):
+            step(k)
+        stream.synchronize()
+        launches_per_step = layer.last_launch_count()
+        path_used = layer.last_path()
+        # clock window + timed region, NVML-sampled
+        sampler = ClockSampler(local)
+        sampler.start()
+        t_end = time.perf_counter() + args.clock_window
+        k = 0
+        while time.perf_counter() < t_end:
+            step(k)
+            k += 1
+            if k % 256 == 0:
+                stream.synchronize()
+        stream.synchronize()
+        barrier(ws)
+        torch.cuda.synchronize()
+        el = time_steps(step, args.steps, stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+        sampler.stop()
+    el_max = max_over_ranks(ws, el)
+    bytes_layer = algorithmic_bytes(d, h, n_m, B)
+    bytes_rank = algorithmic_bytes(d, h_loc, n_m, B)
+    value = bytes_layer * args.steps / el_max / 1e9
+    per_launch_s = el / args.steps / max(1, launches_per_step)
+    peaks = load_peaks()
+    achieved = bytes_rank / per_launch_s / 1e9
+
+    # e2e through the C-ABI host-buffer entry: x H2D + kernel + y D2H every step
+    xh = x.cpu().pin_memory()
+    yh = torch.empty(B, h_loc, dtype=torch.bfloat16).pin_memory()
+
+    def step_host(k):
+        Wt, codes = layers[k % L]
+        layer.forward_host(xh, Wt, codes, yh, stream=stream)
+
+    with torch.cuda.stream(stream):
+        for k in range(max(3, args.warmup)):
+            step_host(k)
+        stream.synchronize()
+        barrier(ws)
+        el_e2e = time_steps(step_host, args.steps, stream)
+        barrier(ws)
+    el_e2e = max_over_ranks(ws, el_e2e)
+    e2e = {"value": bytes_layer * args.steps / el_e2e / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": B * d * 2 * ws, "d2h_bytes_per_step": B * h * 2,
+           "us_per_call": el_e2e / args.steps * 1e6}
+
+    out = None
+    if rank == 0:
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                tr = json.load(f).get(args.workload)
+            if tr:
+                traffic = tr.get("dram_bytes_per_launch")
+        out = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el_max / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (device-drawn, seeded: x~N(0,1), Wt~U(+-1/sqrt(d)), codes i.i.d. Bernoulli(0.5) bits)",
+            "config": {"workload": desc, "d": d, "h": h, "n_m": n_m, "batch": B, "act": act,
+                       "parallelism": f"column-shard h/{ws}" if ws > 1 else "single GPU",
+                       "l2": f"inputs larger than L2: {L} distinct layer copies ({L * bytes_rank / 1e6:.0f} MB/rank) rotated, no flush",
+                       "kernel_path": path_used, "launch": "PDL (programmatic dependent launch) per call"},
+            "us_per_call": el_max / args.steps * 1e6,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                         "peak_source": peaks["source"] + " hbm_gbs (copy)",
+                         "algorithmic_bytes_per_launch": bytes_rank},
+            "e2e": e2e,
+            "gpu_launches": args.steps * launches_per_step,
+            "clocks": sampler.summary(),
+        }
+        if not args.no_comparator and ws == 1:
+            cb = cublas_swiglu_us(d, h, B, L, args.steps, stream)
+            out["cublas_swiglu"] = {"us_per_call": cb["best_us"], "two_gemm_us": cb["two_gemm"],
+                                    "concat_gemm_us": cb["concat_gemm"],
+                                    "mglu_speedup": cb["best_us"] / out["us_per_call"],
+                                    "bytes_per_call": 2 * h * d * 2 + B * d * 2 + B * h * 2}
+        if not args.no_cpu_baseline and ws == 1:
+            from oracle import ACT_NAMES
+            out["cpu_baseline"] = cpu_baseline(d, h, n_m, B, ACT_NAMES[act], budget_s=args.cpu_budget)
+    layer.close()
+    return out
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["mglu", "reference"], default="mglu")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
+    ap.add_argument("--path", choices=["auto", "mma", "simt", "tcgen05"], default="auto")
+    ap.add_argument("--layers", type=int, default=4, help="distinct layer copies rotated (L2 hygiene)")
+    ap.add_argument("--clock-window", type=float, default=0.3)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-comparator", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shape", default=None, help="experiment: d,h,n_m,B (overrides --workload)")
+    args = ap.parse_args(argv)
+    if args.shape:
+        d_, h_, nm_, b_ = (int(v) for v in args.shape.split(","))
+        WORKLOADS["custom"] = (d_, h_, nm_, b_, "swish", f"custom d={d_} h={h_} n_m={nm_} B={b_}")
+        args.workload = "custom"
+    if args.warmup < 3:
+        args.warmup = 3
+    ws, rank, local = (1, 0, 0)
+    if args.impl == "reference":
+        ws = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        out = run_reference(args, ws, rank)
+    else:
+        ws, rank, local = dist_init()
+        out = run_mglu(args, ws, rank, local)
+    if out is not None and rank == 0:
+        print(json.dumps(out))
+    if ws > 1 and args.impl != "reference":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

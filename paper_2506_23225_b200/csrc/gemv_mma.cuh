@@ -1,265 +1,277 @@
-// gemv_mma.cuh -- register-masked tensor-core fused masked GEMV (decode regime, bf16, B <= 8).
+// gemv_mma.cuh -- TMA-fed, register-masked tensor-core fused masked GEMV (decode regime, bf16,
+// 1 <= B <= 8).  MGLU_PATH_MMA.
 //
 // The FlashMGLU forward of Alg. 1 for small B, re-designed for sm_100a:
-//  * a2: W (Wt rows) and the packed codes stream HBM -> registers exactly once per call (P:245,
-//    P:435) with 256-bit / 64-bit coalesced L1-bypassing loads; each CTA owns a contiguous,
-//    byte-balanced range of Wt rows (no split-K across CTAs, no atomics: reading R9);
-//  * a3/a4: instead of per-element predicated adds, the n_m masked operands M_i (.) W are built
-//    in registers (one PRMT sign-replicate + one LOP3 per bf16 pair and mask) and fed, with the
-//    unmasked W, to mma.sync m16n8k16 (bf16 in, fp32 accumulate), x being the B operand.  So
-//    t = x W and s_i = x (M_i (.) W) are accumulated in one pass; the products are
-//    exact in fp32 and the 8-token N dimension serves B <= 8 at the same ALU cost;
-//  * a5: the K range of a 16-row tile is split across the CTA's warps and reduced through shared
-//    memory in a fixed order (deterministic), then
-//  * a6/a7: value_i = t - s_i and y = sum_i g(s_i) value_i (Eq. 3) are applied on chip and
-//    y is stored once as bf16.
+//  * a2: W (rows of Wt) and the packed codes stream HBM -> shared memory exactly once per call
+//    (P:245).  Each CTA owns a contiguous, row-balanced range of Wt rows (no split-K across
+//    CTAs, no atomics: reading R9).  Its rows are processed in rounds of up to 64 rows; a stage of
+//    a round is one 3-D TMA box of W (64-column blocks x rows, 128B-swizzled) plus one box of the
+//    codes, landing in a multi-stage mbarrier ring fed by one producer thread.
+//  * a3/a4: 16 consumer warps.  A round of T 8-row tiles gives each tile WPT = 16 / T warps, each
+//    owning 128 columns of every stage, so the last (ragged) round keeps all warps busy.  The n_m
+//    masked operands M_i (.) W are built in registers from the codes (one PRMT sign-replicate +
+//    one LOP3 per bf16 pair and mask) and fed, with the unmasked W, to mma.sync m16n8k16 (bf16
+//    in, fp32 accumulate) with x as the B operand: t = x W and s_i = x (M_i (.) W) in one pass
+//    (P:217-223).  Products are exact in fp32.
+//  * a5: k is reduced in each warp's MMA accumulators over the row, then across the WPT warps of
+//    a tile through shared memory in a fixed order (deterministic);
+//  * a6/a7: value_i = t - s_i and y = sum_i g(s_i) value_i (Eq. 3) run on registers and y is
+//    stored once as bf16.
 //
-// Logical/physical K permutation: the reduction order over k is free, so each thread loads 16
-// contiguous elements per row (one 32-byte load) and feeds them to four k16 MMA steps; x is read
-// with the same permutation, so every product W[j,k] x[k] is formed with the same k.
+// Pair-role mapping (why one 16-byte LDS feeds one A fragment): the order of the reduction over
+// k is free.  MMA row g (< 8) carries the EVEN bf16 pairs of real row pi(g) and MMA row g + 8 the
+// ODD pairs of the same row; the B operand carries x's even pairs in column 2b and odd pairs in
+// column 2b + 1 for token b.  Thread (g, c)'s A fragment {A[g][2c..], A[g+8][2c..], A[g][2c+8..],
+// A[g+8][2c+8..]} is then the four consecutive pairs 4c..4c+3 of a 32-column step of row pi(g),
+// and y(row pi(g), token b) = D[g][2b] + D[g+8][2b+1], both held by thread (g, b).  The tile row
+// order pi(g) = g/2 + 4 (g mod 2) makes the swizzled 16-byte reads bank-conflict free.
+//
+// PDL: the producer starts streaming W/codes (constant weights) before griddepcontrol.wait; x and
+// out are touched only after it.
 #pragma once
 #include "common.cuh"
+#include "mma_mask.cuh"
+#include "tma.cuh"
 
 namespace mglu {
 
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-  uint32_t d;
-  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
-  return d;
-}
+constexpr int kDecConsumers = 16;                      // consumer warps
+constexpr int kDecThreads = (kDecConsumers + 1) * 32;  // + 1 producer warp
+constexpr int kDecWBytes = 32 * 1024;                  // W region of a stage slot
 
-__device__ __forceinline__ void mma_16816(float (&acc)[4], uint32_t a0, uint32_t a1, uint32_t a2,
-                                          uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
+// code bytes of one 128-column block of a row (the TMA box inner span; also the swizzle span)
+template <int NM> __host__ __device__ constexpr int dec_code_span() { return 16 * NM; }
+// stage slot = W region (32 KB) + codes region (64 rows x 256 columns x NM bits at most)
+template <int NM> __host__ __device__ constexpr int dec_stage_bytes() { return kDecWBytes + 64 * 256 * NM / 8; }
 
-// 32-bit AND-mask for the bf16 pair (elements 2Q, 2Q+1 of a thread's 16) under mask I (0-based):
-// low half = 0xffff iff bit I of code(2Q), high half = 0xffff iff bit I of code(2Q+1).
-// Codes of the 16 elements form a 16*NM-bit string cw[] (element e, mask I at bit NM*e + I).
-// Shift the bit to the MSB of its byte, then PRMT with sign-replicate selectors (bit 3 of each
-// selector nibble) copies that MSB over two bytes.
-template <int NM, int Q, int I>
-__device__ __forceinline__ uint32_t mask_word(const uint32_t* cw) {
-  constexpr int b0 = NM * (2 * Q) + I, b1 = NM * (2 * Q + 1) + I;
-  constexpr int w0 = b0 >> 5, w1 = b1 >> 5;
-  constexpr int sh0 = 7 - (b0 & 7), sh1 = 7 - (b1 & 7);
-  constexpr uint32_t y0 = (b0 & 31) >> 3, y1 = (b1 & 31) >> 3;
-  constexpr uint32_t sel = (8u | y0) | ((8u | y0) << 4) | ((12u | y1) << 8) | ((12u | y1) << 12);
-  return prmt(cw[w0] << sh0, cw[w1] << sh1, sel);
-}
+// round geometry: T tiles of 8 rows, WPT warps per tile, stage width 128 * WPT columns
+__host__ __device__ constexpr int dec_wpt(int tiles) { return kDecConsumers / tiles; }
 
-constexpr int kCodeWords(int nm) { return nm >= 2 ? nm / 2 : 1; }   // u32 words of 16 codes
-
-struct MmaStage {
-  uint32_t wa[8], wb[8];   // 16 bf16 of rows r and r+8 (pairs)
-  uint32_t ca[4], cb[4];   // their 16 codes (16*NM bits)
-};
-
-template <int NM>
-__device__ __forceinline__ void load_codes16(const uint8_t* p, uint32_t (&c)[4]) {
-  if constexpr (NM == 1) { c[0] = ld_nc_u16(p); }
-  else if constexpr (NM == 2) { c[0] = ld_nc_u32(p); }
-  else if constexpr (NM == 4) { uint2 v = ld_nc_v2(p); c[0] = v.x; c[1] = v.y; }
-  else { uint4 v = ld_nc_v4(p); c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w; }
-}
-
-__device__ __forceinline__ void ld_nc_v8(const void* p, uint32_t (&w)[8]) {
-  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
-               : "l"(p));
-}
-
-struct MmaParams {
+struct DecParams {
   const __nv_bfloat16* x;
-  const __nv_bfloat16* Wt;
-  const uint8_t* codes;
   __nv_bfloat16* out;
   int B, d, h;
   int rows_base, rows_rem;   // CTA c owns rows_base + (c < rows_rem) rows
-  int wk_log2;               // K-split: WK = 1 << wk_log2 warps share a tile, WM = 16 / WK
-  int Bp;                    // tokens padded to 1/2/4/8 (partials layout)
+  int stages;                // ring depth
+  int xpar;                  // u32 words per parity array of one token's x in smem (+ pad)
+  int rem_a, rem_b;          // last-round rows of CTAs owning rows_base / rows_base + 1 rows
 };
 
-constexpr int kMmaWarps = 16;
+// swizzled byte offset within a 1024-aligned region of `rb`-byte rows (rb in {16..128})
+__device__ __forceinline__ uint32_t swz(uint32_t lin, uint32_t rb) {
+  return lin ^ (((lin >> 7) & (rb / 16 - 1)) << 4);
+}
 
-template <int NM, int ACT>
-__global__ void __launch_bounds__(kMmaWarps * 32, 1)
-gemv_mma_kernel(const MmaParams p) {
-  extern __shared__ __align__(16) uint8_t smem[];
+template <int NM, int ACT, int NB>
+__global__ void __launch_bounds__(kDecThreads, 1)
+gemv_mma_kernel(const DecParams p,
+                const __grid_constant__ CUtensorMap mW64, const __grid_constant__ CUtensorMap mC64,
+                const __grid_constant__ CUtensorMap mWa, const __grid_constant__ CUtensorMap mCa,
+                const __grid_constant__ CUtensorMap mWb, const __grid_constant__ CUtensorMap mCb) {
+  constexpr int SPAN = dec_code_span<NM>();
+  constexpr int SB = dec_stage_bytes<NM>();
+  constexpr int NACC = NB * (NM + 1);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int S = p.stages;
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB);
+  uint64_t* empty = full + S;
+  float* part = reinterpret_cast<float*>(empty + S);     // [16 warps][32 lanes][NACC]
+  uint32_t* xs = reinterpret_cast<uint32_t*>(part + kDecConsumers * 32 * NACC);
+
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = lane >> 2, c = lane & 3;
-  const int WK = 1 << p.wk_log2, WM = kMmaWarps >> p.wk_log2;
-  const int wk = warp & (WK - 1), wm = warp >> p.wk_log2;
-  const int d = p.d, B = p.B, Bp = p.Bp;
   const int cta = blockIdx.x;
   const int r0 = cta * p.rows_base + min(cta, p.rows_rem);
   const int nrows = p.rows_base + (cta < p.rows_rem ? 1 : 0);
-  const int ntiles = (nrows + 15) >> 4;
-  const int rounds = (ntiles + WM - 1) / WM;
-  const int nch = d >> 6;              // 64-element chunks per row (d % 64 == 0 on this path)
-  const int nkw = nch >> p.wk_log2;    // chunks per warp per tile
-  const int n_items = rounds * nkw;
+  const int d = p.d;
+  const int nfull = nrows >> 6, rem = nrows & 63;
+  const int nks_full = (d + 255) / 256;
+  const int t_rem = (rem + 7) >> 3;
+  const int wpt_rem = rem ? dec_wpt(t_rem) : 1;
+  const int nks_rem = rem ? (d + 128 * wpt_rem - 1) / (128 * wpt_rem) : 0;
+  const int nstages = nfull * nks_full + nks_rem;
 
-  const int xstride = d + 8;                                       // padded smem row (bf16)
-  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smem);
-  float* part = reinterpret_cast<float*>(smem + (size_t)Bp * xstride * 2);
-  // part[wm][wk][a][16 rows][Bp]
-  const int part_acc_stride = 16 * Bp;
-  const int part_warp_stride = (NM + 1) * part_acc_stride;
-
-  auto item_tile = [&](int i) { return (i / nkw) * WM + wm; };
-  auto item_kc = [&](int i) { return wk * nkw + (i % nkw); };
-
-  auto load_stage = [&](MmaStage& s, int i) {
-    const int tile = item_tile(i);
-    const int kc = item_kc(i);
-    const int k = (kc << 6) + (c << 4);
-    const int ra = tile * 16 + r, rb = ra + 8;                  // rows within the CTA range
-    if (tile < ntiles && ra < nrows) {
-      const size_t e = (size_t)(r0 + ra) * d + k;
-      ld_nc_v8(p.Wt + e, s.wa);
-      load_codes16<NM>(p.codes + e * NM / 8, s.ca);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) s.wa[q] = 0u;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) s.ca[q] = 0u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kDecConsumers);
     }
-    if (tile < ntiles && rb < nrows) {
-      const size_t e = (size_t)(r0 + rb) * d + k;
-      ld_nc_v8(p.Wt + e, s.wb);
-      load_codes16<NM>(p.codes + e * NM / 8, s.cb);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) s.wb[q] = 0u;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) s.cb[q] = 0u;
-    }
-  };
-
-  float acc[NM + 1][4];
-#pragma unroll
-  for (int a = 0; a <= NM; ++a)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) acc[a][v] = 0.f;
-
-  auto compute = [&](const MmaStage& s, int i) {
-    const int kc = item_kc(i);
-    uint32_t xr[8];
-    if (r < B) {
-      const uint4* xp = reinterpret_cast<const uint4*>(xs + (size_t)r * xstride + (kc << 6) + (c << 4));
-      const uint4 x0 = xp[0], x1 = xp[1];
-      xr[0] = x0.x; xr[1] = x0.y; xr[2] = x0.z; xr[3] = x0.w;
-      xr[4] = x1.x; xr[5] = x1.y; xr[6] = x1.z; xr[7] = x1.w;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) xr[q] = 0u;
-    }
-    // t += x W  (unmasked operand)
-#pragma unroll
-    for (int st = 0; st < 4; ++st)
-      mma_16816(acc[0], s.wa[2 * st], s.wb[2 * st], s.wa[2 * st + 1], s.wb[2 * st + 1], xr[2 * st], xr[2 * st + 1]);
-    // s_i += x (M_i (.) W)
-#define MGLU_MASKED_STEP(ST, I)                                                                 \
-    mma_16816(acc[1 + I],                                                                       \
-              s.wa[2 * ST] & mask_word<NM, 2 * ST, I>(s.ca),                                    \
-              s.wb[2 * ST] & mask_word<NM, 2 * ST, I>(s.cb),                                    \
-              s.wa[2 * ST + 1] & mask_word<NM, 2 * ST + 1, I>(s.ca),                            \
-              s.wb[2 * ST + 1] & mask_word<NM, 2 * ST + 1, I>(s.cb), xr[2 * ST], xr[2 * ST + 1]);
-#define MGLU_MASKED_ALL_STEPS(I) \
-    if constexpr (I < NM) { MGLU_MASKED_STEP(0, I) MGLU_MASKED_STEP(1, I) MGLU_MASKED_STEP(2, I) MGLU_MASKED_STEP(3, I) }
-    MGLU_MASKED_ALL_STEPS(0)
-    MGLU_MASKED_ALL_STEPS(1)
-    MGLU_MASKED_ALL_STEPS(2)
-    MGLU_MASKED_ALL_STEPS(3)
-    MGLU_MASKED_ALL_STEPS(4)
-    MGLU_MASKED_ALL_STEPS(5)
-    MGLU_MASKED_ALL_STEPS(6)
-    MGLU_MASKED_ALL_STEPS(7)
-#undef MGLU_MASKED_ALL_STEPS
-#undef MGLU_MASKED_STEP
-  };
-
-  // end of a tile round: stash fragments, reduce across the K-split warps, epilogue, store
-  auto flush = [&](int round) {
-    float* pw = part + (size_t)(wm * WK + wk) * part_warp_stride;
-#pragma unroll
-    for (int a = 0; a <= NM; ++a) {
-      float* pa = pw + a * part_acc_stride;
-      const int t0 = 2 * c, t1 = 2 * c + 1;
-      if (t0 < Bp) { pa[r * Bp + t0] = acc[a][0]; pa[(r + 8) * Bp + t0] = acc[a][2]; }
-      if (t1 < Bp) { pa[r * Bp + t1] = acc[a][1]; pa[(r + 8) * Bp + t1] = acc[a][3]; }
-#pragma unroll
-      for (int v = 0; v < 4; ++v) acc[a][v] = 0.f;
-    }
-    __syncthreads();
-    // WM tiles x 16 rows in this round; warp w reduces rows w, w+16, ...
-    const int tok = lane & 7, grp = lane >> 3;
-    for (int orow = warp; orow < WM * 16; orow += kMmaWarps) {
-      const int twm = orow >> 4, row = orow & 15;
-      const int tile = round * WM + twm;
-      float vals[NM + 1];
-#pragma unroll
-      for (int a = 0; a <= NM; ++a) vals[a] = 0.f;
-      if (tok < Bp) {
-        for (int w2 = grp; w2 < WK; w2 += 4) {          // fixed order: deterministic
-          const float* pp = part + (size_t)(twm * WK + w2) * part_warp_stride + row * Bp + tok;
-#pragma unroll
-          for (int a = 0; a <= NM; ++a) vals[a] += pp[a * part_acc_stride];
-        }
-      }
-#pragma unroll
-      for (int a = 0; a <= NM; ++a) {
-        vals[a] += __shfl_xor_sync(0xffffffffu, vals[a], 8);
-        vals[a] += __shfl_xor_sync(0xffffffffu, vals[a], 16);
-      }
-      const int lrow = tile * 16 + row;
-      if (grp == 0 && tok < B && tile < ntiles && lrow < nrows) {
-        float s[NM];
-#pragma unroll
-        for (int i = 0; i < NM; ++i) s[i] = vals[1 + i];
-        const float y = mglu_epilogue<ACT, NM>(vals[0], s);          // Eq. 3, value = t - s_i
-        p.out[(size_t)tok * p.h + r0 + lrow] = __float2bfloat16_rn(y);
-      }
-    }
-    __syncthreads();
-  };
-
-  MmaStage st0, st1, st2;
-  // W and the codes do not depend on the previous kernel: start streaming before the PDL wait.
-  if (n_items > 0) load_stage(st0, 0);
-  if (n_items > 1) load_stage(st1, 1);
-  pdl_wait();
-  pdl_launch_dependents();
-  // x -> shared memory (B rows, padded stride)
-  {
-    const int vec_per_row = d >> 3;   // 16-byte vectors
-    for (int v = threadIdx.x; v < B * vec_per_row; v += blockDim.x) {
-      const int b = v / vec_per_row, q = v - b * vec_per_row;
-      reinterpret_cast<uint4*>(xs + (size_t)b * xstride)[q] =
-          reinterpret_cast<const uint4*>(p.x + (size_t)b * d)[q];
-    }
+    mbar_fence_init();
   }
   __syncthreads();
+  pdl_launch_dependents();
 
-#define MGLU_ITEM(S_CUR, S_NEXT2)                                        \
-  {                                                                      \
-    if (i + 2 < n_items) load_stage(S_NEXT2, i + 2);                     \
-    compute(S_CUR, i);                                                   \
-    if ((i % nkw) == nkw - 1) flush(i / nkw);                            \
-    if (++i >= n_items) break;                                           \
+  if (warp == kDecConsumers) {
+    // ------------------------------------------------------------ producer (one thread)
+    if (lane == 0) {
+      // full rounds: boxes of 64 rows x (4 W blocks | 2 code blocks); the last round: boxes of
+      // exactly `rem` rows x (2 WPT W blocks | WPT code blocks) -> two TMA ops per stage always,
+      // no over-read of the neighbouring CTA's rows (one descriptor pair per CTA row count)
+      const CUtensorMap* mWr = rem == p.rem_a ? &mWa : &mWb;
+      const CUtensorMap* mCr = rem == p.rem_a ? &mCa : &mCb;
+      prefetch_tmap(&mW64); prefetch_tmap(&mC64);
+      if (rem) { prefetch_tmap(mWr); prefetch_tmap(mCr); }
+      const uint64_t pol = policy_evict_first();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nstages; ++i) {
+        const bool is_full = i < nfull * nks_full;
+        const int rho = is_full ? i / nks_full : nfull;
+        const int ks = is_full ? i - rho * nks_full : i - nfull * nks_full;
+        const int rows = is_full ? 64 : rem;
+        const int wpt = is_full ? 2 : wpt_rem;
+        const int k0 = ks * 128 * wpt;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* wst = ring + (size_t)s * SB;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(rows * wpt * (2 * 128 + SPAN)));
+        tma_load_3d_hint(wst, is_full ? &mW64 : mWr, 0, r0 + rho * 64, k0 / 64, &full[s], pol);
+        tma_load_3d_hint(wst + kDecWBytes, is_full ? &mC64 : mCr, 0, r0 + rho * 64, k0 / 128, &full[s], pol);
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+    }
+    return;
   }
-  int i = 0;
-  if (n_items > 0) {
-    for (;;) {
-      MGLU_ITEM(st0, st2)
-      MGLU_ITEM(st1, st0)
-      MGLU_ITEM(st2, st1)
+
+  // -------------------------------------------------------------- consumers
+  const int g = lane >> 2, c = lane & 3;
+  const int B = p.B;
+  const int prow = (g >> 1) + 4 * (g & 1);                 // pi(g): tile-local real row
+
+  pdl_wait();                                              // x is the predecessor's output
+  {
+    // x -> smem split by bf16-pair parity: xs[b][parity][pair/2], zero-padded past d
+    const int npair = p.xpar * 2 - 16;
+    for (int v = threadIdx.x; v < B * npair; v += kDecConsumers * 32) {
+      const int b = v / npair, q = v - b * npair;
+      uint32_t val = 0u;
+      if (2 * q < d) val = reinterpret_cast<const uint32_t*>(p.x + (size_t)b * d)[q];
+      xs[(size_t)(2 * b + (q & 1)) * p.xpar + (q >> 1)] = val;
     }
   }
-#undef MGLU_ITEM
+  named_bar_sync(1, kDecConsumers * 32);
+
+  float acc[NB][NM + 1][4];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+    for (int a = 0; a <= NM; ++a)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[nb][a][v] = 0.f;
+
+  int s = 0;
+  uint32_t ph = 0;
+  int i = 0;
+  for (int rho = 0; rho < nfull + (rem ? 1 : 0); ++rho) {
+    const bool is_full = rho < nfull;
+    const int rows = is_full ? 64 : rem;
+    const int ntile = is_full ? 8 : t_rem;
+    const int wpt = is_full ? 2 : wpt_rem;
+    const int nks = is_full ? nks_full : nks_rem;
+    const int tl = warp / wpt, kp = warp - tl * wpt;        // tile and column part of this warp
+    const bool live = tl < ntile;                           // warp-uniform
+    const int srow = tl * 8 + prow;                         // row within the round's box
+    for (int ks = 0; ks < nks; ++ks, ++i) {
+      mbar_wait(&full[s], ph);
+      if (live) {
+        const uint8_t* wst = ring + (size_t)s * SB;
+        const uint8_t* cst = wst + kDecWBytes;
+        const int kbase = ks * 128 * wpt + kp * 128;         // global column of this warp's part
+#pragma unroll
+        for (int st = 0; st < 4; ++st) {
+          // A: pairs 4c..4c+3 of the step = one swizzled 16-byte read of W block (2 kp + st/2)
+          const uint32_t wlin = (uint32_t)(((2 * kp + (st >> 1)) * rows + srow) * 128 + (32 * (st & 1) + 8 * c) * 2);
+          const uint4 wq = *reinterpret_cast<const uint4*>(wst + swz(wlin, 128));
+          // codes of the thread's 8 columns: NM bytes of code block kp
+          uint32_t cw[2];
+          {
+            const uint32_t clin = (uint32_t)((kp * rows + srow) * SPAN + (32 * st + 8 * c) * NM / 8);
+            const uint8_t* cp = cst + swz(clin, SPAN);
+            if constexpr (NM == 1) cw[0] = *cp;
+            else if constexpr (NM == 2) cw[0] = *reinterpret_cast<const uint16_t*>(cp);
+            else if constexpr (NM == 4) cw[0] = *reinterpret_cast<const uint32_t*>(cp);
+            else { const uint2 u = *reinterpret_cast<const uint2*>(cp); cw[0] = u.x; cw[1] = u.y; }
+          }
+          // B: x pairs (4c + parity, 4c + 2 + parity) of the step for this lane's column(s)
+          uint32_t xb[NB][2];
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) {
+            const int tok = nb * 4 + (g >> 1);
+            if (tok < B) {
+              const int gp = (kbase + 32 * st + 8 * c) / 2;    // global pair index of pair 4c
+              const uint2 u = *reinterpret_cast<const uint2*>(xs + (size_t)(2 * tok + (g & 1)) * p.xpar + (gp >> 1));
+              xb[nb][0] = u.x; xb[nb][1] = u.y;
+            } else {
+              xb[nb][0] = 0u; xb[nb][1] = 0u;
+            }
+          }
+          // t += x W
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) mma_16816(acc[nb][0], wq.x, wq.y, wq.z, wq.w, xb[nb][0], xb[nb][1]);
+          // s_i += x (M_i (.) W): pair q of the thread's 8 columns is register q of the quad
+#define MGLU_MASKED(I)                                                                              \
+          if constexpr (I < NM) {                                                                  \
+            const uint32_t a0 = wq.x & mask_word<NM, 0, I>(cw), a1 = wq.y & mask_word<NM, 1, I>(cw);  \
+            const uint32_t a2 = wq.z & mask_word<NM, 2, I>(cw), a3 = wq.w & mask_word<NM, 3, I>(cw);  \
+            _Pragma("unroll") for (int nb = 0; nb < NB; ++nb)                                      \
+              mma_16816(acc[nb][1 + I], a0, a1, a2, a3, xb[nb][0], xb[nb][1]);                      \
+          }
+          MGLU_MASKED(0) MGLU_MASKED(1) MGLU_MASKED(2) MGLU_MASKED(3)
+          MGLU_MASKED(4) MGLU_MASKED(5) MGLU_MASKED(6) MGLU_MASKED(7)
+#undef MGLU_MASKED
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == S) { s = 0; ph ^= 1; }
+    }
+
+    if (live) {
+      // a5: (even pairs, even column) + (odd pairs, odd column) -> one value per (row, token)
+      // and accumulator; parts kp >= 1 hand theirs to part 0 through smem (fixed order)
+      float v[NB][NM + 1];
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int a = 0; a <= NM; ++a) {
+          v[nb][a] = acc[nb][a][0] + acc[nb][a][3];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[nb][a][q] = 0.f;
+        }
+      float* pw = part + ((size_t)warp * 32 + lane) * NACC;
+      if (kp > 0) {
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int a = 0; a <= NM; ++a) pw[nb * (NM + 1) + a] = v[nb][a];
+      }
+      // barrier ids: full rounds pair warps (2 tl, 2 tl + 1) on id 1 + tl; a ragged round with
+      // another grouping uses ids 9 + tl so no id is shared by two groupings in flight
+      const int bar = (is_full || wpt == 2) ? 1 + tl : 9 + tl;
+      named_bar_sync(bar, wpt * 32);
+      if (kp == 0) {
+        for (int q = 1; q < wpt; ++q) {
+          const float* pq = part + ((size_t)(warp + q) * 32 + lane) * NACC;
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+            for (int a = 0; a <= NM; ++a) v[nb][a] += pq[nb * (NM + 1) + a];
+        }
+        const int row = rho * 64 + tl * 8 + prow;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+          const int tok = nb * 4 + c;
+          if (tok < B && row < nrows) {
+            float sv[NM];
+#pragma unroll
+            for (int ii = 0; ii < NM; ++ii) sv[ii] = v[nb][1 + ii];
+            const float y = mglu_epilogue<ACT, NM>(v[nb][0], sv);       // Eq. 3
+            p.out[(size_t)tok * p.h + r0 + row] = __float2bfloat16_rn(y);
+          }
+        }
+      }
+      named_bar_sync(bar, wpt * 32);                        // partials are rewritten next round
+    }
+  }
 }
 
 }  // namespace mglu

@@ -7,6 +7,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -34,6 +36,17 @@ struct mglu_ctx {
   void* y_stage = nullptr;
   size_t y_stage_bytes = 0;
   mglu::TcState tc;
+  // TMA descriptor cache of the decode path
+  struct DecMaps {
+    bool valid = false;
+    const void* Wt = nullptr;
+    const void* codes = nullptr;
+    uint64_t stamp = 0;
+    CUtensorMap maps[6];
+  };
+  std::array<DecMaps, 16> dec_cache;
+  uint64_t dec_clock = 0;
+
 };
 
 namespace {
@@ -115,40 +128,149 @@ cudaError_t simt_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const vo
   }
 }
 
-// ------------------------------------------------------------------ MMA dispatch
+// ------------------------------------------------------------------ MMA (TMA-fed decode) dispatch
 bool mma_can_serve(const mglu_ctx* hd, int64_t B) {
-  return hd->dtype == MGLU_BF16 && hd->d % 64 == 0 && B >= 1 && B <= 8 && hd->d <= 16384;
+  // 128-column code blocks of 16 * n_m bytes tile the rows exactly
+  return hd->dtype == MGLU_BF16 && hd->d % 128 == 0 && B >= 1 && B <= 8 && hd->d <= 32768;
 }
 
-size_t mma_smem_bytes(const mglu_ctx* hd, int Bp) {
-  return (size_t)Bp * (hd->d + 8) * 2 + (size_t)mglu::kMmaWarps * (hd->n_m + 1) * 16 * Bp * 4;
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encoder() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  });
+  return fn;
+}
+
+// 2-D row-major [rows][cols] tensor of `esize`-byte elements, box (bcols x brows)
+bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* base, uint64_t cols,
+               uint64_t rows, uint32_t bcols, uint32_t brows,
+               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
+  EncodeTiledFn enc = get_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * esize};
+  cuuint32_t box[2] = {bcols, brows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+CUtensorMapSwizzle swizzle_for(int span) {
+  return span == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : span == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+}
+
+// 3-D row-major view [blocks][rows][inner] of a [rows][cols] tensor: inner = `inner` elements of
+// `esize` bytes, blocks of `inner` columns (stride inner*esize), rows (stride cols*esize)
+bool encode_3d_blocks(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* base, uint64_t cols,
+                      uint64_t rows, uint32_t inner, uint32_t brows, uint32_t bblocks, CUtensorMapSwizzle swz) {
+  EncodeTiledFn enc = get_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {inner, rows, cols / inner};
+  cuuint64_t strides[2] = {cols * esize, inner * esize};
+  cuuint32_t box[3] = {inner, brows, bblocks};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// descriptor cache keyed by (Wt, codes).  W: 64-column blocks (SW128); codes: 128-column blocks of
+// 16*n_m bytes (swizzle = span).  Boxes: full rounds 64 rows x (4 | 2) blocks; the last round of
+// CTAs owning rows_base / rows_base + 1 rows: rem_a / rem_b rows x (2 wpt | wpt) blocks.
+bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, int rem_a, int rem_b, CUtensorMap* out6) {
+  std::lock_guard<std::mutex> g(hd->mu);
+  for (auto& e : hd->dec_cache)
+    if (e.valid && e.Wt == Wt && e.codes == codes) {
+      e.stamp = ++hd->dec_clock;
+      memcpy(out6, e.maps, sizeof(e.maps));
+      return true;
+    }
+  const int NM = hd->n_m;
+  const int span = 16 * NM;
+  const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
+  const auto csw = span == 16 ? CU_TENSOR_MAP_SWIZZLE_NONE : swizzle_for(span);
+  const uint64_t crow_u32 = (uint64_t)hd->d * NM / 32;
+  auto wpt_of = [](int rem) { return rem ? mglu::dec_wpt((rem + 7) / 8) : 1; };
+  const int ra = rem_a ? rem_a : 1, rb = rem_b ? rem_b : 1;
+  CUtensorMap m[6];
+  bool ok =
+      encode_3d_blocks(&m[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, 64, 4, sw) &&
+      encode_3d_blocks(&m[1], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, 64, 2, csw) &&
+      encode_3d_blocks(&m[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, ra, 2 * wpt_of(rem_a), sw) &&
+      encode_3d_blocks(&m[3], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, ra, wpt_of(rem_a), csw) &&
+      encode_3d_blocks(&m[4], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, rb, 2 * wpt_of(rem_b), sw) &&
+      encode_3d_blocks(&m[5], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, rb, wpt_of(rem_b), csw);
+  if (!ok) return false;
+  size_t victim = 0;
+  for (size_t i = 0; i < hd->dec_cache.size(); ++i) {
+    if (!hd->dec_cache[i].valid) { victim = i; break; }
+    if (hd->dec_cache[i].stamp < hd->dec_cache[victim].stamp) victim = i;
+  }
+  auto& e = hd->dec_cache[victim];
+  e.valid = true; e.Wt = Wt; e.codes = codes; e.stamp = ++hd->dec_clock;
+  memcpy(e.maps, m, sizeof(m));
+  memcpy(out6, m, sizeof(m));
+  return true;
+}
+
+template <int NM, int ACT, int NB>
+cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
+                       void* out, cudaStream_t st) {
+  mglu::DecParams p;
+  p.x = (const __nv_bfloat16*)x;
+  p.out = (__nv_bfloat16*)out;
+  p.B = B;
+  p.d = (int)hd->d;
+  p.h = (int)hd->h;
+  int64_t ncta = (hd->h + 7) / 8;
+  if (ncta > hd->num_sms) ncta = hd->num_sms;
+  p.rows_base = (int)(hd->h / ncta);
+  p.rows_rem = (int)(hd->h % ncta);
+  p.rem_a = p.rows_base & 63;
+  p.rem_b = (p.rows_base + 1) & 63;
+  CUtensorMap maps[6];
+  if (!dec_maps(hd, Wt, codes, p.rem_a, p.rem_b, maps)) return cudaErrorInvalidValue;
+  // x in smem, split by pair parity and zero-padded to the last column any stage can touch
+  int64_t maxcol = (hd->d + 255) / 256 * 256;
+  for (int rem : {p.rem_a, p.rem_b}) {
+    if (!rem) continue;
+    const int64_t ks = 128 * (int64_t)mglu::dec_wpt((rem + 7) / 8);
+    maxcol = std::max<int64_t>(maxcol, (hd->d + ks - 1) / ks * ks);
+  }
+  const int npair = (int)(maxcol / 2);
+  p.xpar = npair / 2 + 8;
+  constexpr size_t SB = mglu::dec_stage_bytes<NM>();
+  const size_t xbytes = (size_t)2 * B * p.xpar * 4;
+  const size_t partbytes = (size_t)mglu::kDecConsumers * 32 * NB * (NM + 1) * 4;
+  const size_t fixed = xbytes + partbytes + 1024;
+  const size_t cap = std::min<size_t>((size_t)hd->max_smem_optin, 200 * 1024);
+  if (cap < fixed) return cudaErrorInvalidConfiguration;
+  int S = (int)((cap - fixed) / (SB + 16));
+  S = std::min(8, S);
+  if (S < 2) return cudaErrorInvalidConfiguration;
+  p.stages = S;
+  const size_t smem = (size_t)S * SB + 2 * S * sizeof(uint64_t) + partbytes + xbytes;
+  auto kern = mglu::gemv_mma_kernel<NM, ACT, NB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(kern, dim3((unsigned)ncta), dim3(mglu::kDecThreads), smem, st, p, maps[0], maps[1], maps[2],
+                    maps[3], maps[4], maps[5]);
 }
 
 template <int NM, int ACT>
 cudaError_t run_mma(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
                     void* out, cudaStream_t st) {
-  mglu::MmaParams p;
-  p.x = (const __nv_bfloat16*)x;
-  p.Wt = (const __nv_bfloat16*)Wt;
-  p.codes = (const uint8_t*)codes;
-  p.out = (__nv_bfloat16*)out;
-  p.B = B;
-  p.d = (int)hd->d;
-  p.h = (int)hd->h;
-  p.Bp = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
-  int64_t ncta = (hd->h + 15) / 16;
-  if (ncta > hd->num_sms) ncta = hd->num_sms;
-  p.rows_base = (int)(hd->h / ncta);
-  p.rows_rem = (int)(hd->h % ncta);
-  const int nch = (int)(hd->d / 64);
-  int wkl = 0;
-  while (wkl < 4 && (nch % (1 << (wkl + 1))) == 0) ++wkl;   // WK = largest pow2 <= 16 | nch
-  p.wk_log2 = wkl;
-  const size_t smem = mma_smem_bytes(hd, p.Bp);
-  auto kern = mglu::gemv_mma_kernel<NM, ACT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(kern, dim3((unsigned)ncta), dim3(mglu::kMmaWarps * 32), smem, st, p);
+  return B <= 4 ? run_mma_nb<NM, ACT, 1>(hd, x, B, Wt, codes, out, st)
+                : run_mma_nb<NM, ACT, 2>(hd, x, B, Wt, codes, out, st);
 }
 
 template <int NM>
@@ -279,7 +401,7 @@ mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* W
   if (path == MGLU_PATH_MMA) {
     if (!mma_can_serve(hd, B)) {
       if (prev != hd->device) cudaSetDevice(prev);
-      return set_err(hd, MGLU_ERR_UNSUPPORTED, "MMA path needs bf16, d % 64 == 0, 1 <= B <= 8");
+      return set_err(hd, MGLU_ERR_UNSUPPORTED, "MMA path needs bf16, 1 <= B <= 8, d % 128 == 0");
     }
     e = mma_nm(hd, x, (int)B, Wt, packed, out, st);
     launches = 1;

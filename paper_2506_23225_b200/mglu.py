@@ -240,6 +240,22 @@ class Mglu:
 
     __call__ = forward
 
+    def bind(self, x, Wt, packed, out, stream=None):
+        """Validate once and return a zero-argument callable that enqueues mglu_forward with
+        the pointers pre-marshalled (the per-call host cost is one ctypes call)."""
+        self._check_inputs(x, Wt, packed)
+        lib = load_library()
+        B = x.shape[0] if x.dim() == 2 else 1
+        args = (self.handle, x.data_ptr(), B, Wt.data_ptr(), packed.data_ptr(), out.data_ptr(),
+                _stream_ptr(stream, x.device))
+        fwd = lib.mglu_forward
+
+        def call():
+            st = fwd(*args)
+            if st != MGLU_OK:
+                _check(st, self.handle, "mglu_forward")
+        return call
+
     def forward_partials(self, x, Wt, packed, stream=None) -> torch.Tensor:
         self._check_inputs(x, Wt, packed)
         B = x.shape[0]

@@ -43,6 +43,13 @@ SHAPES = [  # (d, h, B) -- several tiles, ragged row tails, B up to the MMA grou
 @pytest.mark.parametrize("path", ["mma", "simt"])
 def test_bf16_shapes(n_m, d, h, B, path):
     inp = make_inputs(1000 + n_m * 7 + d + h + B, B=B, d=d, h=h, n_m=n_m, dtype="bf16")
+    if path == "mma" and d % 128:
+        # the MMA path tiles rows in 128-column code blocks (16 * n_m bytes): d % 128 == 0
+        from paper_2506_23225_b200.mglu import MgluError, MGLU_ERR_UNSUPPORTED
+        with pytest.raises(MgluError) as e:
+            gpu_forward(inp, "bf16", n_m, "swish", path=path)
+        assert e.value.status == MGLU_ERR_UNSUPPORTED
+        return
     y, used = gpu_forward(inp, "bf16", n_m, "swish", path=path)
     assert used == path
     ref = oracle_forward(inp, "bf16", n_m, "swish")
