@@ -21,12 +21,15 @@
  *   x        [B][d]   dtype of the handle (bf16 or f32)
  *   Wt       [h][d]   dtype of the handle.  Row j is column j of the logical W (d x h), i.e.
  *                     Alg. 1's A and nn.Linear.weight.
- *   packed   h*d*n_m/8 bytes: the dense code layout (reading R3).  Element (j,k)'s
- *                     n_m-bit code c[j,k] occupies stream bits [n_m*(j*d+k), n_m*(j*d+k)+n_m);
- *                     stream bit q is bit (q mod 8) of byte q/8 (little-endian).  Mask M_i is bit
- *                     (i-1) of the code (Alg. 1: "mask[row,k] AND (1 << (i-1))").
- *                     Rows of Wt own contiguous byte ranges [j*d*n_m/8, (j+1)*d*n_m/8), so an
- *                     h-shard of a layer is a pointer offset into Wt and into packed.
+ *   packed   h*d*n_m/8 bytes (n_m bits per weight, Table 1's n_m*hd), the pair-split
+ *                     bit-plane layout of DESIGN.md reading R3: for row j, 32-column group
+ *                     g = k/32 and mask i (1..n_m), one little-endian 32-bit word at byte offset
+ *                     ((j*(d/32) + g)*n_m + (i-1))*4 holds M_i[j, 32g .. 32g+31], column 32g+e at
+ *                     bit (e/2) + 16*(e mod 2) (even columns in the low half-word, odd columns in
+ *                     the high half-word).  M_i is bit (i-1) of the element's n_m-bit code
+ *                     (Alg. 1: "mask[row,k] AND (1 << (i-1))").  Rows of Wt own contiguous
+ *                     byte ranges [j*d*n_m/8, (j+1)*d*n_m/8), so an h-shard of a layer is a
+ *                     pointer offset into Wt and into packed.
  *   out      [B][h]   dtype of the handle; bf16 stored round-to-nearest-even from fp32.
  *   z        [B][2*n_m][h] fp32 (debug partials, Alg. 1's accumulator order P:208):
  *                     z[b][i-1][j] = gate_i = s_i,   z[b][n_m+i-1][j] = value_i = t - s_i.
@@ -61,7 +64,7 @@ typedef struct mglu_ctx* mglu_handle;
 typedef enum {
   MGLU_OK = 0,
   MGLU_ERR_INVALID_ARG = 1,   /* null pointer, negative size, bad enum, dtype mismatch       */
-  MGLU_ERR_UNSUPPORTED = 2,   /* n_m not in {1,2,4,8}; d % 8 != 0; path not available for cfg */
+  MGLU_ERR_UNSUPPORTED = 2,   /* n_m not in {1,2,4,8}; d % 32 != 0; path not available for cfg*/
   MGLU_ERR_MISALIGNED = 3,    /* a data pointer not 16-byte aligned                           */
   MGLU_ERR_CUDA = 4,          /* a CUDA runtime/driver call failed; see mglu_last_error()     */
   MGLU_ERR_OOM = 5            /* workspace allocation failed                                  */
@@ -89,9 +92,9 @@ typedef enum {
 } mglu_path;
 
 /* Create a handle for one (d, h, n_m, act, dtype) layer on CUDA device `device`.
- *   d, h >= 1; d % 8 == 0 (8 elements = n_m whole bytes of codes, 16-byte row alignment);
- *   n_m in {1, 2, 4, 8} (dense byte-aligned code widths, reading R3).
- * Errors: INVALID_ARG (null out, bad enum, d/h < 1), UNSUPPORTED (n_m, d % 8), CUDA, OOM. */
+ *   d, h >= 1; d % 32 == 0 (the 32-column groups of the packed layout, reading R3);
+ *   n_m in {1, 2, 4, 8}.
+ * Errors: INVALID_ARG (null out, bad enum, d/h < 1), UNSUPPORTED (n_m, d % 32), CUDA, OOM. */
 mglu_status mglu_create(mglu_handle* out, int64_t d, int64_t h, int n_m, int act, int dtype,
                         int device);
 
@@ -121,14 +124,15 @@ mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, cons
 mglu_status mglu_forward_host(mglu_handle hd, const void* x_host, int64_t B, const void* Wt,
                               const void* packed, void* out_host, void* stream);
 
-/* Number of packed-code bytes of an (h x d) layer with n_m masks: ceil(h*d*n_m/8) (Table 1's
- * n_m*hd mask bits).  Returns 0 for invalid arguments. */
+/* Number of packed-mask bytes of an (h x d) layer with n_m masks: h*d*n_m/8 (Table 1's n_m*hd
+ * mask bits).  Returns 0 for invalid arguments (including d % 32 != 0). */
 size_t mglu_packed_mask_bytes(int64_t d, int64_t h, int n_m);
 
 /* Offline mask packing ("all masks are fixed"; "Combine the n_m binary masks ...").
  *   bits   [n_m][h][d] uint8, each 0 or 1 (INVALID_ARG on any other value)
  *   logits [n_m][h][d] float32; bit = (logit > 0), strict (Alg. 2; reading R4)
- *   packed mglu_packed_mask_bytes(d, h, n_m) bytes (written entirely)
+ *   packed mglu_packed_mask_bytes(d, h, n_m) bytes (written entirely); d % 32 == 0 else
+ *          UNSUPPORTED; device variants need a 16-byte aligned packed buffer (MISALIGNED)
  * Host variants work on host memory, run synchronously and validate every bit byte; device
  * variants take device pointers, enqueue one kernel on `stream` and use bit (b & 1) of each byte
  * (a device-side value check could only be reported after a synchronisation). */

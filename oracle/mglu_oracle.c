@@ -17,10 +17,12 @@
  * value_i is computed as its own dot product with the complementary mask -- NOT as t - gate_i
  * (that identity, is what the kernel exploits and what the tests check).
  *
- * Mask bits (reading R3, dense codes): M_i[j,k] is bit (i-1) of the n_m-bit code
- * c[j,k] (Alg. 1 bit test "mask[row,k] AND (1 << (i-1))").  The codes are stored densely:
- * code c[j,k] occupies bits [n_m*(j*d+k), n_m*(j*d+k)+n_m) of the packed stream, where bit q of
- * the stream is bit (q mod 8) of byte floor(q/8) (little-endian).  This file reads that layout
+ * Mask bits (reading R3): M_i[j,k] is bit (i-1) of the n_m-bit code c[j,k] (Alg. 1
+ * bit test "mask[row,k] AND (1 << (i-1))"), stored densely (n_m bits per weight, Table 1
+ * P:278) in the pair-split bit-plane layout: for row j, column group g = k / 32 and mask i, one
+ * little-endian 32-bit word at byte offset ((j*(d/32) + g)*n_m + (i-1))*4 holds the 32 bits of
+ * M_i[j, 32g .. 32g+31]; column 32g + e sits at bit (e / 2) + 16*(e mod 2) (even columns in the
+ * low half-word, odd columns in the high half-word).  d % 32 == 0.  This file reads that layout
  * with its own bit-at-a-time loop, independent of the library's packer.
  *
  * g (reading R5): 0 identity, 1 swish z*sigmoid(z) (beta=1), 2 gelu 0.5 z (1+erf(z/sqrt2)),
@@ -41,15 +43,20 @@
 #include <omp.h>
 #endif
 
-/* bit q of the little-endian packed stream */
-static int stream_bit(const uint8_t *packed, uint64_t q) {
-    return (packed[q / 8u] >> (q % 8u)) & 1;
+/* byte offset of the word holding M_i[j, 32g .. 32g+31] and the bit of column k in it */
+static uint64_t word_offset(int n_m, int64_t d, int64_t j, int64_t k, int i) {
+    uint64_t g = (uint64_t)k / 32u;
+    return (((uint64_t)j * ((uint64_t)d / 32u) + g) * (uint64_t)n_m + (uint64_t)(i - 1)) * 4u;
+}
+static unsigned bit_in_word(int64_t k) {
+    unsigned e = (unsigned)(k % 32);
+    return e / 2u + 16u * (e % 2u);
 }
 
-/* M_i[j,k] for i = 1..n_m, read bit by bit from the dense code layout */
+/* M_i[j,k] for i = 1..n_m: byte (bit / 8) of the little-endian word, bit (bit mod 8) */
 static int mask_bit(const uint8_t *packed, int n_m, int64_t d, int64_t j, int64_t k, int i) {
-    uint64_t field = (uint64_t)n_m * ((uint64_t)j * (uint64_t)d + (uint64_t)k);
-    return stream_bit(packed, field + (uint64_t)(i - 1));
+    unsigned b = bit_in_word(k);
+    return (packed[word_offset(n_m, d, j, k, i) + b / 8u] >> (b % 8u)) & 1;
 }
 
 static double act_g(int act, double z) {
@@ -71,25 +78,24 @@ int oracle_num_threads(void) {
 #endif
 }
 
-/* bits[(i-1)][j][k] in {0,1}  ->  packed stream (h*d*n_m/8 bytes, caller-zeroed not required) */
+/* bits[(i-1)][j][k] in {0,1}  ->  packed layout (h*d*n_m/8 bytes) */
 int oracle_pack(const uint8_t *bits, int n_m, int64_t h, int64_t d, uint8_t *packed) {
-    if (n_m < 1 || n_m > 8 || h < 0 || d < 0) return 1;
-    uint64_t nbits = (uint64_t)n_m * (uint64_t)h * (uint64_t)d;
-    memset(packed, 0, (size_t)((nbits + 7u) / 8u));
+    if (n_m < 1 || n_m > 8 || h < 0 || d < 0 || d % 32) return 1;
+    memset(packed, 0, (size_t)((uint64_t)n_m * (uint64_t)h * (uint64_t)d / 8u));
     for (int64_t j = 0; j < h; ++j)
         for (int64_t k = 0; k < d; ++k)
             for (int i = 1; i <= n_m; ++i) {
                 uint8_t b = bits[((uint64_t)(i - 1) * (uint64_t)h + (uint64_t)j) * (uint64_t)d + (uint64_t)k];
                 if (b > 1) return 2;
-                uint64_t q = (uint64_t)n_m * ((uint64_t)j * (uint64_t)d + (uint64_t)k) + (uint64_t)(i - 1);
-                if (b) packed[q / 8u] |= (uint8_t)(1u << (q % 8u));
+                unsigned q = bit_in_word(k);
+                if (b) packed[word_offset(n_m, d, j, k, i) + q / 8u] |= (uint8_t)(1u << (q % 8u));
             }
     return 0;
 }
 
-/* packed stream -> bits[(i-1)][j][k] */
+/* packed layout -> bits[(i-1)][j][k] */
 int oracle_unpack(const uint8_t *packed, int n_m, int64_t h, int64_t d, uint8_t *bits) {
-    if (n_m < 1 || n_m > 8 || h < 0 || d < 0) return 1;
+    if (n_m < 1 || n_m > 8 || h < 0 || d < 0 || d % 32) return 1;
     for (int i = 1; i <= n_m; ++i)
         for (int64_t j = 0; j < h; ++j)
             for (int64_t k = 0; k < d; ++k)
@@ -102,7 +108,7 @@ int oracle_unpack(const uint8_t *packed, int n_m, int64_t h, int64_t d, uint8_t 
  * Eq. 3 for the token rows x[0..B) and the output columns cols[0..ncols).
  *   x      [B][d]        binary64 (bf16/f32 inputs decoded exactly by the caller)
  *   Wt_sel [ncols][d]    binary64, row c is Wt[cols[c], :]
- *   packed full packed-mask stream of the (h x d) layer (global column index cols[c] is used)
+ *   packed full packed-mask buffer of the (h x d) layer (global row index cols[c] is used)
  *   y      [B][ncols]    output
  *   z      [B][2*n_m][ncols] or NULL: Alg. 1's accumulator order:
  *          row (i-1) = gate_i, row (n_m+i-1) = value_i
@@ -112,7 +118,7 @@ int oracle_mglu_forward(const double *x, int64_t B, int64_t d,
                         const double *Wt_sel, const int64_t *cols, int64_t ncols,
                         const uint8_t *packed, int n_m, int act,
                         double *y, double *z, double *t_out) {
-    if (n_m < 1 || n_m > 8 || act < 0 || act > 4 || B < 0 || d < 0 || ncols < 0) return 1;
+    if (n_m < 1 || n_m > 8 || act < 0 || act > 4 || B < 0 || d < 0 || d % 32 || ncols < 0) return 1;
     int64_t c;
 #pragma omp parallel for schedule(dynamic, 8)
     for (c = 0; c < ncols; ++c) {

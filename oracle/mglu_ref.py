@@ -44,14 +44,25 @@ def decode_bf16(u16: np.ndarray) -> np.ndarray:
     return u.view(np.float32).astype(np.float64)
 
 
+def _bit_of_column(d: int) -> np.ndarray:
+    """Reading R3: column 32g + e of a group sits at bit (e // 2) + 16 * (e % 2) of its word."""
+    e = np.arange(d) % 32
+    return (e // 2) + 16 * (e % 2)
+
+
 def unpack_np(packed: np.ndarray, n_m: int, h: int, d: int) -> np.ndarray:
-    """Dense code layout (reading R3): the n_m-bit code of element (j,k) sits at stream bits
-    [n_m*(j*d+k), +n_m), stream bit q = bit (q mod 8) of byte q//8; mask i is bit (i-1) of the
-    code (Alg. 1).  Returns bits[i-1][j][k] in {0,1}."""
-    stream = np.unpackbits(np.asarray(packed, dtype=np.uint8), bitorder="little")
-    stream = stream[: n_m * h * d]
-    codes_bits = stream.reshape(h, d, n_m)          # [...,i-1] = bit (i-1) of code (j,k)
-    return np.ascontiguousarray(np.transpose(codes_bits, (2, 0, 1)))
+    """Pair-split bit-plane layout (reading R3): for row j, 32-column group g and mask i, one
+    little-endian uint32 word (word index (j*(d/32) + g)*n_m + i-1) holds M_i[j, 32g..32g+31], column
+    32g+e at bit (e//2) + 16*(e%2).  Mask i is bit (i-1) of the code (Alg. 1, P:221).
+    Returns bits[i-1][j][k] in {0,1}."""
+    if d % 32:
+        raise ValueError("d must be a multiple of 32")
+    words = np.frombuffer(np.ascontiguousarray(packed, dtype=np.uint8).tobytes(), dtype="<u4")
+    words = words[: h * (d // 32) * n_m].reshape(h, d // 32, n_m)      # [j][g][i-1]
+    per_col = np.repeat(words, 32, axis=1)                               # [j][k][i-1] (word of column k)
+    shifts = _bit_of_column(d).astype(np.uint32)[None, :, None]
+    bits = (per_col >> shifts) & np.uint32(1)
+    return np.ascontiguousarray(np.transpose(bits, (2, 0, 1)).astype(np.uint8))
 
 
 def pack_np(bits: np.ndarray) -> np.ndarray:
@@ -60,8 +71,12 @@ def pack_np(bits: np.ndarray) -> np.ndarray:
     if bits.max(initial=0) > 1:
         raise ValueError("mask entries must be 0/1")
     n_m, h, d = bits.shape
-    stream = np.transpose(bits, (1, 2, 0)).reshape(-1)
-    return np.packbits(stream, bitorder="little")
+    if d % 32:
+        raise ValueError("d must be a multiple of 32")
+    weights = (np.uint64(1) << _bit_of_column(d).astype(np.uint64))        # value of column k's bit
+    contrib = np.transpose(bits, (1, 2, 0)).astype(np.uint64) * weights[None, :, None]   # [j][k][i]
+    words = contrib.reshape(h, d // 32, 32, n_m).sum(axis=2).astype("<u4")               # [j][g][i]
+    return np.frombuffer(words.tobytes(), dtype=np.uint8).copy()
 
 
 def mglu_partials_np(x: np.ndarray, Wt: np.ndarray, bits: np.ndarray):

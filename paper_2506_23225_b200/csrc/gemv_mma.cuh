@@ -9,12 +9,13 @@
 //    codes, landing in a multi-stage mbarrier ring fed by one producer thread.
 //  * a3/a4: 16 consumer warps.  A round of T 8-row tiles gives each tile WPT = 16 / T warps, each
 //    owning 128 columns of every stage, so the last (ragged) round keeps all warps busy.  The n_m
-//    masked operands M_i (.) W are built in registers from the codes (one PRMT sign-replicate +
-//    one LOP3 per bf16 pair and mask) and fed, with the unmasked W, to mma.sync m16n8k16 (bf16
-//    in, fp32 accumulate) with x as the B operand: t = x W and s_i = x (M_i (.) W) in one pass
-//    (P:217-223).  Products are exact in fp32.
+//    masked operands are built in registers from the mask words as sign-flipped copies
+//    sigma_i (.) W (one IMAD + one LOP3 per bf16 pair and mask, see sign_flip) and fed, with the
+//    unmasked W, to mma.sync m16n8k16 (bf16 in, fp32 accumulate) with x as the B operand:
+//    t = x W and u_i = x (sigma_i (.) W) = s_i - v_i in one pass, so
+//    s_i = (t + u_i) / 2 = x (M_i (.) W) and v_i = t - s_i.  Products are exact in fp32.
 //  * a5: k is reduced in each warp's MMA accumulators over the row, then across the WPT warps of
-//    a tile through shared memory in a fixed order (deterministic);
+//    a tile through shared memory in a fixed order at the end of the round (deterministic);
 //  * a6/a7: value_i = t - s_i and y = sum_i g(s_i) value_i (Eq. 3) run on registers and y is
 //    stored once as bf16.
 //
@@ -35,14 +36,16 @@
 
 namespace mglu {
 
-constexpr int kDecConsumers = 16;                      // consumer warps
+constexpr int kDecConsumers = 16;                      // consumer warps (4 per SM sub-partition)
 constexpr int kDecThreads = (kDecConsumers + 1) * 32;  // + 1 producer warp
-constexpr int kDecWBytes = 32 * 1024;                  // W region of a stage slot
+constexpr int kDecFullTiles = kDecConsumers / 2;       // 8-row tiles of a full round (2 warps each)
+constexpr int kDecFullRows = 8 * kDecFullTiles;        // 64
+constexpr int kDecWBytes = kDecConsumers * 2048;       // W region of a stage slot (max over rounds)
 
-// code bytes of one 128-column block of a row (the TMA box inner span; also the swizzle span)
+// mask bytes of one 128-column block of a row: 4 groups x n_m words (TMA box inner span = swizzle span)
 template <int NM> __host__ __device__ constexpr int dec_code_span() { return 16 * NM; }
-// stage slot = W region (32 KB) + codes region (64 rows x 256 columns x NM bits at most)
-template <int NM> __host__ __device__ constexpr int dec_stage_bytes() { return kDecWBytes + 64 * 256 * NM / 8; }
+// stage slot = W region + codes region (rows x WPT blocks x 16 NM bytes <= 128 * consumers * NM)
+template <int NM> __host__ __device__ constexpr int dec_stage_bytes() { return kDecWBytes + 128 * kDecConsumers * NM; }
 
 // round geometry: T tiles of 8 rows, WPT warps per tile, stage width 128 * WPT columns
 __host__ __device__ constexpr int dec_wpt(int tiles) { return kDecConsumers / tiles; }
@@ -84,7 +87,7 @@ gemv_mma_kernel(const DecParams p,
   const int r0 = cta * p.rows_base + min(cta, p.rows_rem);
   const int nrows = p.rows_base + (cta < p.rows_rem ? 1 : 0);
   const int d = p.d;
-  const int nfull = nrows >> 6, rem = nrows & 63;
+  const int nfull = nrows / kDecFullRows, rem = nrows - nfull * kDecFullRows;
   const int nks_full = (d + 255) / 256;
   const int t_rem = (rem + 7) >> 3;
   const int wpt_rem = rem ? dec_wpt(t_rem) : 1;
@@ -118,14 +121,14 @@ gemv_mma_kernel(const DecParams p,
         const bool is_full = i < nfull * nks_full;
         const int rho = is_full ? i / nks_full : nfull;
         const int ks = is_full ? i - rho * nks_full : i - nfull * nks_full;
-        const int rows = is_full ? 64 : rem;
+        const int rows = is_full ? kDecFullRows : rem;
         const int wpt = is_full ? 2 : wpt_rem;
         const int k0 = ks * 128 * wpt;
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* wst = ring + (size_t)s * SB;
         mbar_arrive_expect_tx(&full[s], (uint32_t)(rows * wpt * (2 * 128 + SPAN)));
-        tma_load_3d_hint(wst, is_full ? &mW64 : mWr, 0, r0 + rho * 64, k0 / 64, &full[s], pol);
-        tma_load_3d_hint(wst + kDecWBytes, is_full ? &mC64 : mCr, 0, r0 + rho * 64, k0 / 128, &full[s], pol);
+        tma_load_3d_hint(wst, is_full ? &mW64 : mWr, 0, r0 + rho * kDecFullRows, k0 / 64, &full[s], pol);
+        tma_load_3d_hint(wst + kDecWBytes, is_full ? &mC64 : mCr, 0, r0 + rho * kDecFullRows, k0 / 128, &full[s], pol);
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
@@ -136,6 +139,11 @@ gemv_mma_kernel(const DecParams p,
   const int g = lane >> 2, c = lane & 3;
   const int B = p.B;
   const int prow = (g >> 1) + 4 * (g & 1);                 // pi(g): tile-local real row
+  // pair q of this thread's 8 columns = group columns 8c + 2q, 8c + 2q + 1 -> layout bits
+  // 4c + q and 16 + 4c + q; multiplying by 2^(15 - 4c - q) moves them to bits 15 and 31
+  uint32_t mul[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) mul[q] = 1u << (15 - 4 * c - q);
 
   pdl_wait();                                              // x is the predecessor's output
   {
@@ -163,8 +171,8 @@ gemv_mma_kernel(const DecParams p,
   int i = 0;
   for (int rho = 0; rho < nfull + (rem ? 1 : 0); ++rho) {
     const bool is_full = rho < nfull;
-    const int rows = is_full ? 64 : rem;
-    const int ntile = is_full ? 8 : t_rem;
+    const int rows = is_full ? kDecFullRows : rem;
+    const int ntile = is_full ? kDecFullTiles : t_rem;
     const int wpt = is_full ? 2 : wpt_rem;
     const int nks = is_full ? nks_full : nks_rem;
     const int tl = warp / wpt, kp = warp - tl * wpt;        // tile and column part of this warp
@@ -181,15 +189,20 @@ gemv_mma_kernel(const DecParams p,
           // A: pairs 4c..4c+3 of the step = one swizzled 16-byte read of W block (2 kp + st/2)
           const uint32_t wlin = (uint32_t)(((2 * kp + (st >> 1)) * rows + srow) * 128 + (32 * (st & 1) + 8 * c) * 2);
           const uint4 wq = *reinterpret_cast<const uint4*>(wst + swz(wlin, 128));
-          // codes of the thread's 8 columns: NM bytes of code block kp
-          uint32_t cw[2];
+          // mask words of this step's 32-column group (group st of code block kp): n_m words
+          uint32_t mw[NM];
           {
-            const uint32_t clin = (uint32_t)((kp * rows + srow) * SPAN + (32 * st + 8 * c) * NM / 8);
-            const uint8_t* cp = cst + swz(clin, SPAN);
-            if constexpr (NM == 1) cw[0] = *cp;
-            else if constexpr (NM == 2) cw[0] = *reinterpret_cast<const uint16_t*>(cp);
-            else if constexpr (NM == 4) cw[0] = *reinterpret_cast<const uint32_t*>(cp);
-            else { const uint2 u = *reinterpret_cast<const uint2*>(cp); cw[0] = u.x; cw[1] = u.y; }
+            const uint32_t clin = (uint32_t)((kp * rows + srow) * SPAN + st * 4 * NM);
+#pragma unroll
+            for (int q = 0; q < (NM + 3) / 4; ++q) {
+              const uint8_t* cp = cst + swz(clin + 16 * q, SPAN);
+              if constexpr (NM == 1) mw[0] = *reinterpret_cast<const uint32_t*>(cp);
+              else if constexpr (NM == 2) { const uint2 u = *reinterpret_cast<const uint2*>(cp); mw[0] = u.x; mw[1] = u.y; }
+              else {
+                const uint4 u = *reinterpret_cast<const uint4*>(cp);
+                mw[4 * q] = u.x; mw[4 * q + 1] = u.y; mw[4 * q + 2] = u.z; mw[4 * q + 3] = u.w;
+              }
+            }
           }
           // B: x pairs (4c + parity, 4c + 2 + parity) of the step for this lane's column(s)
           uint32_t xb[NB][2];
@@ -207,17 +220,14 @@ gemv_mma_kernel(const DecParams p,
           // t += x W
 #pragma unroll
           for (int nb = 0; nb < NB; ++nb) mma_16816(acc[nb][0], wq.x, wq.y, wq.z, wq.w, xb[nb][0], xb[nb][1]);
-          // s_i += x (M_i (.) W): pair q of the thread's 8 columns is register q of the quad
-#define MGLU_MASKED(I)                                                                              \
-          if constexpr (I < NM) {                                                                  \
-            const uint32_t a0 = wq.x & mask_word<NM, 0, I>(cw), a1 = wq.y & mask_word<NM, 1, I>(cw);  \
-            const uint32_t a2 = wq.z & mask_word<NM, 2, I>(cw), a3 = wq.w & mask_word<NM, 3, I>(cw);  \
-            _Pragma("unroll") for (int nb = 0; nb < NB; ++nb)                                      \
-              mma_16816(acc[nb][1 + I], a0, a1, a2, a3, xb[nb][0], xb[nb][1]);                      \
+          // u_i += x (sigma_i (.) W): pair q of the thread's 8 columns is register q of the quad
+#pragma unroll
+          for (int ii = 0; ii < NM; ++ii) {
+            const uint32_t a0 = sign_flip(wq.x, mw[ii], mul[0]), a1 = sign_flip(wq.y, mw[ii], mul[1]);
+            const uint32_t a2 = sign_flip(wq.z, mw[ii], mul[2]), a3 = sign_flip(wq.w, mw[ii], mul[3]);
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) mma_16816(acc[nb][1 + ii], a0, a1, a2, a3, xb[nb][0], xb[nb][1]);
           }
-          MGLU_MASKED(0) MGLU_MASKED(1) MGLU_MASKED(2) MGLU_MASKED(3)
-          MGLU_MASKED(4) MGLU_MASKED(5) MGLU_MASKED(6) MGLU_MASKED(7)
-#undef MGLU_MASKED
         }
       }
       __syncwarp();
@@ -225,52 +235,48 @@ gemv_mma_kernel(const DecParams p,
       if (++s == S) { s = 0; ph ^= 1; }
     }
 
-    if (live) {
-      // a5: (even pairs, even column) + (odd pairs, odd column) -> one value per (row, token)
-      // and accumulator; parts kp >= 1 hand theirs to part 0 through smem (fixed order)
-      float v[NB][NM + 1];
+    // a5: (even pairs, even column) + (odd pairs, odd column) -> one value per (row, token)
+    // and accumulator; parts kp >= 1 hand theirs to part 0 through smem (fixed order).  The round
+    // ends at the same stage for every warp, so one consumer-wide barrier pair serves all tiles.
+    float v[NB][NM + 1];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int a = 0; a <= NM; ++a) {
+        v[nb][a] = acc[nb][a][0] + acc[nb][a][3];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[nb][a][q] = 0.f;
+      }
+    if (live && kp > 0) {
+      float* pw = part + ((size_t)warp * 32 + lane) * NACC;
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-        for (int a = 0; a <= NM; ++a) {
-          v[nb][a] = acc[nb][a][0] + acc[nb][a][3];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[nb][a][q] = 0.f;
-        }
-      float* pw = part + ((size_t)warp * 32 + lane) * NACC;
-      if (kp > 0) {
+        for (int a = 0; a <= NM; ++a) pw[nb * (NM + 1) + a] = v[nb][a];
+    }
+    named_bar_sync(1, kDecConsumers * 32);                  // the producer keeps streaming meanwhile
+    if (live && kp == 0) {
+      for (int q = 1; q < wpt; ++q) {
+        const float* pq = part + ((size_t)(warp + q) * 32 + lane) * NACC;
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-          for (int a = 0; a <= NM; ++a) pw[nb * (NM + 1) + a] = v[nb][a];
+          for (int a = 0; a <= NM; ++a) v[nb][a] += pq[nb * (NM + 1) + a];
       }
-      // barrier ids: full rounds pair warps (2 tl, 2 tl + 1) on id 1 + tl; a ragged round with
-      // another grouping uses ids 9 + tl so no id is shared by two groupings in flight
-      const int bar = (is_full || wpt == 2) ? 1 + tl : 9 + tl;
-      named_bar_sync(bar, wpt * 32);
-      if (kp == 0) {
-        for (int q = 1; q < wpt; ++q) {
-          const float* pq = part + ((size_t)(warp + q) * 32 + lane) * NACC;
+      const int row = rho * kDecFullRows + tl * 8 + prow;
 #pragma unroll
-          for (int nb = 0; nb < NB; ++nb)
+      for (int nb = 0; nb < NB; ++nb) {
+        const int tok = nb * 4 + c;
+        if (tok < B && row < nrows) {
+          float sv[NM];
 #pragma unroll
-            for (int a = 0; a <= NM; ++a) v[nb][a] += pq[nb * (NM + 1) + a];
-        }
-        const int row = rho * 64 + tl * 8 + prow;
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
-          const int tok = nb * 4 + c;
-          if (tok < B && row < nrows) {
-            float sv[NM];
-#pragma unroll
-            for (int ii = 0; ii < NM; ++ii) sv[ii] = v[nb][1 + ii];
-            const float y = mglu_epilogue<ACT, NM>(v[nb][0], sv);       // Eq. 3
-            p.out[(size_t)tok * p.h + r0 + row] = __float2bfloat16_rn(y);
-          }
+          for (int ii = 0; ii < NM; ++ii) sv[ii] = 0.5f * (v[nb][0] + v[nb][1 + ii]);   // s_i = (t + u_i) / 2
+          const float y = mglu_epilogue<ACT, NM>(v[nb][0], sv);       // Eq. 3, value = t - s_i
+          p.out[(size_t)tok * p.h + r0 + row] = __float2bfloat16_rn(y);
         }
       }
-      named_bar_sync(bar, wpt * 32);                        // partials are rewritten next round
     }
+    named_bar_sync(1, kDecConsumers * 32);                  // partials are rewritten next round
   }
 }
 

@@ -14,7 +14,7 @@
 
 namespace mglu {
 
-// Eight consecutive elements of one row: weights as fp32, their codes as one 8*NM-bit word.
+// Eight consecutive elements of one row (weights or x) as fp32.
 template <typename T> struct Row8;
 template <> struct Row8<__nv_bfloat16> {
   __device__ static void load(const __nv_bfloat16* p, float (&w)[8]) {
@@ -40,13 +40,12 @@ template <> struct Row8<float> {
   }
 };
 
-// codes of 8 consecutive elements: NM bytes at byte offset (j*d + k)*NM/8 (d % 8 == 0)
+// Mask words of the 32-column group holding 8 consecutive elements (reading R3 layout): n_m
+// little-endian u32 words, column 32g + e of mask i at bit (e >> 1) + 16*(e & 1) of word i.
 template <int NM>
-__device__ __forceinline__ uint64_t load_codes8(const uint8_t* p) {
-  if constexpr (NM == 1) return ld_nc_u8(p);
-  else if constexpr (NM == 2) return ld_nc_u16(p);
-  else if constexpr (NM == 4) return ld_nc_u32(p);
-  else { uint2 v = ld_nc_v2(p); return (uint64_t)v.x | ((uint64_t)v.y << 32); }
+__device__ __forceinline__ void load_group_words(const uint32_t* p, uint32_t (&w)[NM]) {
+#pragma unroll
+  for (int i = 0; i < NM; ++i) w[i] = ld_nc_u32(p + i);
 }
 
 constexpr int kSimtTok = 4;   // tokens accumulated per pass over a row
@@ -62,7 +61,7 @@ gemv_simt_kernel(const T* __restrict__ x, int B, int d, const T* __restrict__ Wt
   const int ngroups = d >> 3;   // 8-element groups per row
   for (int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < h; j += warps_total) {
     const T* wrow = Wt + (size_t)j * d;
-    const uint8_t* crow = codes + (size_t)j * d * NM / 8;
+    const uint32_t* crow = reinterpret_cast<const uint32_t*>(codes) + (size_t)j * (d / 32) * NM;
     for (int b0 = 0; b0 < B; b0 += kSimtTok) {
       const int nb = min(kSimtTok, B - b0);
       float t[kSimtTok], s[kSimtTok][NM];
@@ -75,7 +74,9 @@ gemv_simt_kernel(const T* __restrict__ x, int B, int d, const T* __restrict__ Wt
       for (int g = lane; g < ngroups; g += 32) {
         float w[8];
         Row8<T>::load(wrow + g * 8, w);
-        const uint64_t c = load_codes8<NM>(crow + (size_t)g * NM);
+        uint32_t cw[NM];
+        load_group_words<NM>(crow + (size_t)(g >> 2) * NM, cw);
+        const int e0 = (g & 3) * 8;                         // first column of the 8 in the group
 #pragma unroll
         for (int b = 0; b < kSimtTok; ++b) {
           if (b < nb) {
@@ -85,10 +86,10 @@ gemv_simt_kernel(const T* __restrict__ x, int B, int d, const T* __restrict__ Wt
             for (int e = 0; e < 8; ++e) {
               const float v = w[e] * xv[e];                 // P:218 v = A[row,k] * x[k]
               t[b] += v;                                    // P:219 t = t + v
-              const uint32_t ce = (uint32_t)(c >> (NM * e));
+              const int bit = ((e0 + e) >> 1) + 16 * (e & 1);   // e0 even
 #pragma unroll
               for (int i = 0; i < NM; ++i)                  // P:220-222 bit test, s_i += v
-                if (ce & (1u << i)) s[b][i] += v;
+                if ((cw[i] >> bit) & 1u) s[b][i] += v;
             }
           }
         }

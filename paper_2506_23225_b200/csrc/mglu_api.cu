@@ -151,20 +151,6 @@ EncodeTiledFn get_encoder() {
   return fn;
 }
 
-// 2-D row-major [rows][cols] tensor of `esize`-byte elements, box (bcols x brows)
-bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* base, uint64_t cols,
-               uint64_t rows, uint32_t bcols, uint32_t brows,
-               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
-  EncodeTiledFn enc = get_encoder();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * esize};
-  cuuint32_t box[2] = {bcols, brows};
-  cuuint32_t es[2] = {1, 1};
-  return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 CUtensorMapSwizzle swizzle_for(int span) {
   return span == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : span == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
 }
@@ -202,9 +188,10 @@ bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, int rem_a, int re
   auto wpt_of = [](int rem) { return rem ? mglu::dec_wpt((rem + 7) / 8) : 1; };
   const int ra = rem_a ? rem_a : 1, rb = rem_b ? rem_b : 1;
   CUtensorMap m[6];
+  const uint32_t fr = mglu::kDecFullRows;
   bool ok =
-      encode_3d_blocks(&m[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, 64, 4, sw) &&
-      encode_3d_blocks(&m[1], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, 64, 2, csw) &&
+      encode_3d_blocks(&m[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, fr, 4, sw) &&
+      encode_3d_blocks(&m[1], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, fr, 2, csw) &&
       encode_3d_blocks(&m[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, ra, 2 * wpt_of(rem_a), sw) &&
       encode_3d_blocks(&m[3], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, ra, wpt_of(rem_a), csw) &&
       encode_3d_blocks(&m[4], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, rb, 2 * wpt_of(rem_b), sw) &&
@@ -235,8 +222,8 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   if (ncta > hd->num_sms) ncta = hd->num_sms;
   p.rows_base = (int)(hd->h / ncta);
   p.rows_rem = (int)(hd->h % ncta);
-  p.rem_a = p.rows_base & 63;
-  p.rem_b = (p.rows_base + 1) & 63;
+  p.rem_a = p.rows_base % mglu::kDecFullRows;
+  p.rem_b = (p.rows_base + 1) % mglu::kDecFullRows;
   CUtensorMap maps[6];
   if (!dec_maps(hd, Wt, codes, p.rem_a, p.rem_b, maps)) return cudaErrorInvalidValue;
   // x in smem, split by pair parity and zero-padded to the last column any stage can touch
@@ -308,6 +295,36 @@ mglu_status check_ptrs(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, c
 
 }  // namespace
 
+// ------------------------------------------------------------------ packing helpers
+static void put_le32(uint8_t* p, uint32_t v) {
+  p[0] = (uint8_t)v; p[1] = (uint8_t)(v >> 8); p[2] = (uint8_t)(v >> 16); p[3] = (uint8_t)(v >> 24);
+}
+static uint32_t get_le32(const uint8_t* p) {
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+
+template <typename BitOf>
+static void pack_words(int n_m, int64_t h, int64_t d, uint8_t* packed, BitOf bit_of) {
+  const int64_t groups = d / 32;
+  for (int64_t j = 0; j < h; ++j)
+    for (int64_t g = 0; g < groups; ++g)
+      for (int i = 0; i < n_m; ++i) {
+        uint32_t v = 0;
+        for (int e = 0; e < 32; ++e) v |= bit_of(i, j, g * 32 + e) << mglu::code_bit_of(e);
+        put_le32(packed + ((j * groups + g) * n_m + i) * 4, v);
+      }
+}
+
+static mglu_status device_launch_check(cudaError_t e) {
+  return e == cudaSuccess ? MGLU_OK : MGLU_ERR_CUDA;
+}
+
+static unsigned grid_for(int64_t n) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  return (unsigned)std::max<int64_t>(1, blocks);
+}
+
 extern "C" {
 
 const char* mglu_version(void) { return "0.1.0"; }
@@ -324,8 +341,8 @@ const char* mglu_last_error(mglu_handle hd) {
 }
 
 size_t mglu_packed_mask_bytes(int64_t d, int64_t h, int n_m) {
-  if (d < 0 || h < 0 || !valid_nm(n_m)) return 0;
-  return (size_t)((h * d * n_m + 7) / 8);
+  if (d < 0 || h < 0 || !valid_nm(n_m) || d % 32) return 0;
+  return (size_t)(h * d * n_m / 8);
 }
 
 mglu_status mglu_create(mglu_handle* out, int64_t d, int64_t h, int n_m, int act, int dtype,
@@ -334,7 +351,7 @@ mglu_status mglu_create(mglu_handle* out, int64_t d, int64_t h, int n_m, int act
   *out = nullptr;
   if (d < 1 || h < 1 || act < 0 || act > 4 || (dtype != MGLU_BF16 && dtype != MGLU_F32) || device < 0)
     return MGLU_ERR_INVALID_ARG;
-  if (!valid_nm(n_m) || d % 8 != 0 || h > ((int64_t)1 << 31) - 1 || d > ((int64_t)1 << 24))
+  if (!valid_nm(n_m) || d % 32 != 0 || h > ((int64_t)1 << 31) - 1 || d > ((int64_t)1 << 24))
     return MGLU_ERR_UNSUPPORTED;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) return MGLU_ERR_CUDA;
@@ -482,98 +499,71 @@ mglu_status mglu_forward_host(mglu_handle hd, const void* x_host, int64_t B, con
 }
 
 // ------------------------------------------------------------------ packing
+// Layout (reading R3, include/mglu.h): row j, 32-column group g, mask i -> little-endian u32 word
+// (j*(d/32) + g)*n_m + i; column 32g + e at bit (e >> 1) + 16*(e & 1).
 mglu_status mglu_pack_masks_host(const uint8_t* bits, int n_m, int64_t h, int64_t d, uint8_t* packed) {
   if (!bits || !packed || h < 0 || d < 0) return MGLU_ERR_INVALID_ARG;
-  if (!valid_nm(n_m)) return MGLU_ERR_UNSUPPORTED;
+  if (!valid_nm(n_m) || d % 32) return MGLU_ERR_UNSUPPORTED;
   const int64_t hd = h * d;
-  const int per = 8 / n_m;
-  const int64_t nbytes = (hd * n_m + 7) / 8;
-  for (int64_t byte = 0; byte < nbytes; ++byte) {
-    uint32_t v = 0;
-    for (int q = 0; q < per; ++q) {
-      const int64_t e = byte * per + q;
-      if (e >= hd) break;
-      for (int i = 0; i < n_m; ++i) {
-        const uint8_t b = bits[(int64_t)i * hd + e];
-        if (b > 1) return MGLU_ERR_INVALID_ARG;
-        v |= (uint32_t)b << (q * n_m + i);
-      }
-    }
-    packed[byte] = (uint8_t)v;
-  }
+  for (int64_t q = 0; q < (int64_t)n_m * hd; ++q)
+    if (bits[q] > 1) return MGLU_ERR_INVALID_ARG;
+  pack_words(n_m, h, d, packed, [&](int i, int64_t j, int64_t k) { return (uint32_t)bits[i * hd + j * d + k]; });
   return MGLU_OK;
 }
 
 mglu_status mglu_pack_logits_host(const float* logits, int n_m, int64_t h, int64_t d, uint8_t* packed) {
   if (!logits || !packed || h < 0 || d < 0) return MGLU_ERR_INVALID_ARG;
-  if (!valid_nm(n_m)) return MGLU_ERR_UNSUPPORTED;
+  if (!valid_nm(n_m) || d % 32) return MGLU_ERR_UNSUPPORTED;
   const int64_t hd = h * d;
-  const int per = 8 / n_m;
-  const int64_t nbytes = (hd * n_m + 7) / 8;
-  for (int64_t byte = 0; byte < nbytes; ++byte) {
-    uint32_t v = 0;
-    for (int q = 0; q < per; ++q) {
-      const int64_t e = byte * per + q;
-      if (e >= hd) break;
-      for (int i = 0; i < n_m; ++i)
-        v |= (logits[(int64_t)i * hd + e] > 0.0f ? 1u : 0u) << (q * n_m + i);   // strict (R4)
-    }
-    packed[byte] = (uint8_t)v;
-  }
+  pack_words(n_m, h, d, packed, [&](int i, int64_t j, int64_t k) {
+    return logits[i * hd + j * d + k] > 0.0f ? 1u : 0u;      // strict (R4)
+  });
   return MGLU_OK;
 }
 
 mglu_status mglu_unpack_masks_host(const uint8_t* packed, int n_m, int64_t h, int64_t d, uint8_t* bits) {
   if (!bits || !packed || h < 0 || d < 0) return MGLU_ERR_INVALID_ARG;
-  if (!valid_nm(n_m)) return MGLU_ERR_UNSUPPORTED;
-  const int64_t hd = h * d;
-  const int per = 8 / n_m;
-  for (int64_t e = 0; e < hd; ++e) {
-    const uint32_t code = (packed[e / per] >> ((e % per) * n_m)) & ((1u << n_m) - 1u);
-    for (int i = 0; i < n_m; ++i) bits[(int64_t)i * hd + e] = (uint8_t)((code >> i) & 1u);
-  }
+  if (!valid_nm(n_m) || d % 32) return MGLU_ERR_UNSUPPORTED;
+  const int64_t hd = h * d, groups = d / 32;
+  for (int64_t j = 0; j < h; ++j)
+    for (int64_t k = 0; k < d; ++k)
+      for (int i = 0; i < n_m; ++i) {
+        const uint32_t w = get_le32(packed + ((j * groups + k / 32) * n_m + i) * 4);
+        bits[i * hd + j * d + k] = (uint8_t)((w >> mglu::code_bit_of((int)(k % 32))) & 1u);
+      }
   return MGLU_OK;
-}
-
-static mglu_status device_launch_check(cudaError_t e) {
-  return e == cudaSuccess ? MGLU_OK : MGLU_ERR_CUDA;
 }
 
 mglu_status mglu_pack_masks_device(const uint8_t* bits, int n_m, int64_t h, int64_t d, uint8_t* packed,
                                    void* stream) {
   if (!bits || !packed || h < 0 || d < 0) return MGLU_ERR_INVALID_ARG;
-  if (!valid_nm(n_m)) return MGLU_ERR_UNSUPPORTED;
-  const int64_t hd = h * d, nbytes = (hd * n_m + 7) / 8;
-  if (nbytes == 0) return MGLU_OK;
-  int64_t blocks = (nbytes + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  // 0/1 validation flag: written only on a bad value; the host cannot see it without a sync,
-  // so the device packer clamps (bit & 1) and documents the host packer as the validating one.
-  mglu::pack_kernel<uint8_t><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(bits, n_m, hd, packed, nbytes, nullptr);
+  if (!valid_nm(n_m) || d % 32) return MGLU_ERR_UNSUPPORTED;
+  if (!aligned16(packed)) return MGLU_ERR_MISALIGNED;
+  const int64_t nwords = h * (d / 32) * n_m;
+  if (nwords == 0) return MGLU_OK;
+  mglu::pack_kernel<uint8_t><<<grid_for(nwords), 256, 0, (cudaStream_t)stream>>>(bits, n_m, h, d, (uint32_t*)packed);
   return device_launch_check(cudaGetLastError());
 }
 
 mglu_status mglu_pack_logits_device(const float* logits, int n_m, int64_t h, int64_t d, uint8_t* packed,
                                     void* stream) {
   if (!logits || !packed || h < 0 || d < 0) return MGLU_ERR_INVALID_ARG;
-  if (!valid_nm(n_m)) return MGLU_ERR_UNSUPPORTED;
-  const int64_t hd = h * d, nbytes = (hd * n_m + 7) / 8;
-  if (nbytes == 0) return MGLU_OK;
-  int64_t blocks = (nbytes + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  mglu::pack_kernel<float><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(logits, n_m, hd, packed, nbytes, nullptr);
+  if (!valid_nm(n_m) || d % 32) return MGLU_ERR_UNSUPPORTED;
+  if (!aligned16(packed)) return MGLU_ERR_MISALIGNED;
+  const int64_t nwords = h * (d / 32) * n_m;
+  if (nwords == 0) return MGLU_OK;
+  mglu::pack_kernel<float><<<grid_for(nwords), 256, 0, (cudaStream_t)stream>>>(logits, n_m, h, d, (uint32_t*)packed);
   return device_launch_check(cudaGetLastError());
 }
 
 mglu_status mglu_unpack_masks_device(const uint8_t* packed, int n_m, int64_t h, int64_t d, uint8_t* bits,
                                      void* stream) {
   if (!bits || !packed || h < 0 || d < 0) return MGLU_ERR_INVALID_ARG;
-  if (!valid_nm(n_m)) return MGLU_ERR_UNSUPPORTED;
+  if (!valid_nm(n_m) || d % 32) return MGLU_ERR_UNSUPPORTED;
+  if (!aligned16(packed)) return MGLU_ERR_MISALIGNED;
   const int64_t hd = h * d;
   if (hd == 0) return MGLU_OK;
-  int64_t blocks = (hd + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  mglu::unpack_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(packed, n_m, hd, bits);
+  mglu::unpack_kernel<<<grid_for(hd), 256, 0, (cudaStream_t)stream>>>((const uint32_t*)packed, n_m, h, d, bits);
   return device_launch_check(cudaGetLastError());
 }
 

@@ -18,24 +18,18 @@ __device__ __forceinline__ void mma_16816(float (&acc)[4], uint32_t a0, uint32_t
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// 32-bit AND-mask for the bf16 pair (elements 2Q, 2Q+1 of a thread's 16) under mask I (0-based):
-// low half = 0xffff iff bit I of code(2Q), high half = 0xffff iff bit I of code(2Q+1).
-// Codes of the 16 elements form a 16*NM-bit string cw[] (element e, mask I at bit NM*e + I).
-// Shift the bit to the MSB of its byte, then PRMT with sign-replicate selectors (bit 3 of each
-// selector nibble) copies that MSB over two bytes.
-template <int NM, int Q, int I>
-__device__ __forceinline__ uint32_t mask_word(const uint32_t* cw) {
-  constexpr int b0 = NM * (2 * Q) + I, b1 = NM * (2 * Q + 1) + I;
-  constexpr int w0 = b0 >> 5, w1 = b1 >> 5;
-  constexpr int sh0 = 7 - (b0 & 7), sh1 = 7 - (b1 & 7);
-  constexpr uint32_t y0 = (b0 & 31) >> 3, y1 = (b1 & 31) >> 3;
-  constexpr uint32_t sel = (8u | y0) | ((8u | y0) << 4) | ((12u | y1) << 8) | ((12u | y1) << 12);
-  return prmt(cw[w0] << sh0, cw[w1] << sh1, sel);
-}
-
-template <int NM>
-__device__ __forceinline__ void codes_from_u4(uint4 v, uint32_t (&c)[4]) {
-  c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
+// Sign-flip masking of a bf16 pair (reading R3 layout).  With sigma = +1 where M_i = 1 (gate)
+// and -1 where M_i = 0 (value), the tensor core accumulates u_i = x (sigma (.) W) = s_i - v_i, and
+// the epilogue recovers s_i = (t + u_i) / 2, v_i = (t - u_i) / 2 (exact rescaling of the same
+// products).  The two mask bits of the pair's columns sit 16 bits apart in the layout word, so
+// ONE multiply (FMA pipe) by 2^(15 - bit) brings them to bf16 sign positions 15 and 31 and ONE
+// LOP3 (ALU pipe) flips the signs of the value-side elements: W ^ (~S & 0x80008000).
+__device__ __forceinline__ uint32_t sign_flip(uint32_t w_pair, uint32_t word, uint32_t mult) {
+  uint32_t sh;
+  // inline PTX keeps this an IMAD on the FMA pipe (a C++ multiply by a known power of two is
+  // strength-reduced to SHF on the ALU pipe, which the LOP3s already load)
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(sh) : "r"(word), "r"(mult));
+  return w_pair ^ (~sh & 0x80008000u);
 }
 
 }  // namespace mglu

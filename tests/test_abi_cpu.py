@@ -40,6 +40,7 @@ def test_packed_bytes(lib):
     assert M.mglu_packed_mask_bytes(4096, 14336, 4) == 14336 * 4096 // 2
     assert M.mglu_packed_mask_bytes(64, 128, 1) == 64 * 128 // 8
     assert M.mglu_packed_mask_bytes(64, 128, 3) == 0
+    assert M.mglu_packed_mask_bytes(48, 128, 4) == 0         # d % 32 != 0
     assert M.mglu_packed_mask_bytes(-1, 128, 1) == 0
 
 
@@ -65,11 +66,9 @@ def test_host_pack_golden(lib, golden_dir):
     cases = json.load(open(os.path.join(golden_dir, "pack_golden.json")))["cases"]
     for case in cases:
         n_m, h, d = case["n_m"], case["h"], case["d"]
-        if "masks" in case:
-            bits = np.array(case["masks"], dtype=np.uint8)
-        else:
-            codes = np.array(case["codes"])
-            bits = np.array([(codes >> i) & 1 for i in range(n_m)], dtype=np.uint8)
+        bits = np.zeros((n_m, h, d), dtype=np.uint8)
+        for i, j, k in case["ones"]:
+            bits[i - 1, j, k] = 1
         assert bytes(M.mglu_pack_masks_host(bits)) == bytes.fromhex(case["packed_hex"])
         back = M.mglu_unpack_masks_host(np.frombuffer(bytes.fromhex(case["packed_hex"]), np.uint8), n_m, h, d)
         np.testing.assert_array_equal(back, bits)
@@ -90,13 +89,16 @@ def test_host_pack_matches_oracle(lib, c_oracle, n_m):
 
 
 def test_host_pack_rejects_non_binary(lib):
-    bits = np.zeros((2, 4, 8), dtype=np.uint8)
+    bits = np.zeros((2, 4, 32), dtype=np.uint8)
     bits[1, 2, 3] = 2
     with pytest.raises(M.MgluError) as e:
         M.mglu_pack_masks_host(bits)
     assert e.value.status == M.MGLU_ERR_INVALID_ARG
     with pytest.raises(M.MgluError) as e:
-        M.mglu_pack_masks_host(np.zeros((3, 4, 8), dtype=np.uint8))
+        M.mglu_pack_masks_host(np.zeros((3, 4, 32), dtype=np.uint8))
+    assert e.value.status == M.MGLU_ERR_UNSUPPORTED
+    with pytest.raises(M.MgluError) as e:                   # d % 32 != 0 (layout groups, R3)
+        M.mglu_pack_masks_host(np.zeros((2, 4, 48), dtype=np.uint8))
     assert e.value.status == M.MGLU_ERR_UNSUPPORTED
 
 

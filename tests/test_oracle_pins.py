@@ -27,15 +27,29 @@ def _load(golden_dir, name):
         return json.load(f)
 
 
+def _pad32(x, Wt, bits):
+    """Zero-pad the reduction dim to a multiple of 32 (the packed layout's group, reading R3):
+    zero columns of W and x add exact zeros to every sum, so Eq. 3 is unchanged."""
+    d = Wt.shape[1]
+    dp = -(-d // 32) * 32
+    if dp == d:
+        return x, Wt, bits
+    pad = dp - d
+    return (np.pad(x, ((0, 0), (0, pad))), np.pad(Wt, ((0, 0), (0, pad))),
+            np.pad(bits, ((0, 0), (0, 0), (0, pad))))
+
+
 def _forward_both(c_oracle, x, Wt, bits, act):
-    """y from the numpy twin and from the C oracle (which sees only the packed stream)."""
+    """y from the numpy twin (on the unpadded inputs) and from the C oracle (which sees only the
+    packed layout, on zero-padded inputs when d % 32 != 0)."""
     x = np.atleast_2d(np.asarray(x, dtype=np.float64))
     Wt = np.asarray(Wt, dtype=np.float64)
     bits = np.asarray(bits, dtype=np.uint8)
     y_np = mglu_forward_np(x, Wt, bits, act)
-    packed = c_oracle.pack(bits)
+    xp, Wp, bp = _pad32(x, Wt, bits)
+    packed = c_oracle.pack(bp)
     h = Wt.shape[0]
-    y_c = c_oracle.forward(x, Wt, np.arange(h), packed, bits.shape[0], act)
+    y_c = c_oracle.forward(xp, Wp, np.arange(h), packed, bits.shape[0], act)
     return y_np, y_c
 
 
@@ -51,9 +65,8 @@ def test_worked_example_2x2(c_oracle, golden_dir, act_name):
         np.testing.assert_allclose(y[0], g["y"][act_name], rtol=1e-15, atol=0)
     t, gate, value = mglu_partials_np(np.array([g["x"]], float), np.array(g["Wt"], float), bits)
     assert t[0].tolist() == g["t"] and gate[0, 0].tolist() == g["gate"] and value[0, 0].tolist() == g["value"]
-    packed = c_oracle.pack(bits)
-    y, z, tc = c_oracle.forward(np.array([g["x"]], float), np.array(g["Wt"], float), np.arange(2),
-                                packed, 1, act, want_partials=True)
+    xp, Wp, bp = _pad32(np.array([g["x"]], float), np.array(g["Wt"], float), bits)
+    y, z, tc = c_oracle.forward(xp, Wp, np.arange(2), c_oracle.pack(bp), 1, act, want_partials=True)
     assert z[0, 0].tolist() == g["gate"] and z[0, 1].tolist() == g["value"] and tc[0].tolist() == g["t"]
 
 
@@ -213,7 +226,7 @@ def test_complementarity(c_oracle, n_m):
     t, gate, value = mglu_partials_np(x, Wt, bits)
     np.testing.assert_allclose(gate + value, np.broadcast_to(t, gate.shape), rtol=1e-13, atol=1e-14)
     _, z, tc = c_oracle.forward(x, Wt, np.arange(24), c_oracle.pack(bits), n_m, ACT_SWISH,
-                                want_partials=True)
+                                want_partials=True)     # d = 96: a multiple of the 32-column group
     np.testing.assert_allclose(z[:, :n_m] + z[:, n_m:], np.repeat(tc[:, None], n_m, 1), rtol=1e-13, atol=1e-14)
     np.testing.assert_allclose(tc, t, rtol=1e-13, atol=1e-14)
 
@@ -259,11 +272,10 @@ def test_decode_bf16_exact():
 
 # ---------------------------------------------------------------- packing (a1)
 def _golden_bits(case):
-    n_m, h, d = case["n_m"], case["h"], case["d"]
-    if "masks" in case:
-        return np.array(case["masks"], dtype=np.uint8)
-    codes = np.array(case["codes"])
-    return np.array([(codes >> i) & 1 for i in range(n_m)], dtype=np.uint8)
+    bits = np.zeros((case["n_m"], case["h"], case["d"]), dtype=np.uint8)
+    for i, j, k in case["ones"]:
+        bits[i - 1, j, k] = 1
+    return bits
 
 
 def test_pack_golden_vectors(c_oracle, golden_dir):
@@ -280,7 +292,7 @@ def test_pack_golden_vectors(c_oracle, golden_dir):
 def test_pack_round_trip(c_oracle, n_m):
     """pack(unpack(p)) = p for random streams; numpy and C unpackers agree."""
     rng = np.random.default_rng(n_m)
-    h, d = 6, 40
+    h, d = 6, 96
     packed = rng.integers(0, 256, size=h * d * n_m // 8, dtype=np.uint8)
     b1 = unpack_np(packed, n_m, h, d)
     b2 = c_oracle.unpack(packed, n_m, h, d)
@@ -297,3 +309,21 @@ def test_binarize_strict_threshold():
     lg = make_logits(0, 2, 64, 64)
     frac = float((lg > 0).mean())
     assert abs(frac - 0.5) < 0.02
+
+
+@pytest.mark.parametrize("n_m", [1, 4])
+def test_layout_bit_positions(c_oracle, n_m):
+    """Reading R3, enumerated: a word with the single bit p set marks exactly column
+    2*(p % 16) + p // 16 of its group (bits 0..15 even columns, 16..31 odd), for every p, every
+    mask word and a second group -- both unpackers."""
+    h, d = 1, 64
+    for g in range(2):
+        for i in range(n_m):
+            for pbit in range(32):
+                words = np.zeros(h * (d // 32) * n_m, dtype="<u4")
+                words[g * n_m + i] = np.uint32(1) << np.uint32(pbit)
+                packed = np.frombuffer(words.tobytes(), dtype=np.uint8)
+                want = np.zeros((n_m, h, d), dtype=np.uint8)
+                want[i, 0, 32 * g + 2 * (pbit % 16) + pbit // 16] = 1
+                np.testing.assert_array_equal(unpack_np(packed, n_m, h, d), want)
+                np.testing.assert_array_equal(c_oracle.unpack(packed, n_m, h, d), want)
