@@ -40,14 +40,38 @@ WORKLOADS = {
     "sweep_b1_nm2": (8192, 28672, 2, 1, "swish", "config5 batch-1 d=8192 h=28672 n_m=2"),
     "sweep_b1_nm4": (8192, 28672, 4, 1, "swish", "config5 batch-1 d=8192 h=28672 n_m=4"),
     "sweep_b1_nm8": (8192, 28672, 8, 1, "swish", "config5 batch-1 d=8192 h=28672 n_m=8"),
+    "prefill": (8192, 28672, 4, 4096, "swish", "config4 prefill SwiMGLU d=8192 h=28672 n_m=4, 4096 tokens"),
+    "decode_b64": (4096, 14336, 4, 64, "swish", "config3 batch-64 SwiMGLU d=4096 h=14336 n_m=4"),
+    "sweep_b2048_nm1": (8192, 28672, 1, 2048, "swish", "config5 batch-2048 d=8192 h=28672 n_m=1"),
+    "sweep_b2048_nm2": (8192, 28672, 2, 2048, "swish", "config5 batch-2048 d=8192 h=28672 n_m=2"),
+    "sweep_b2048_nm4": (8192, 28672, 4, 2048, "swish", "config5 batch-2048 d=8192 h=28672 n_m=4"),
+    "sweep_b2048_nm8": (8192, 28672, 8, 2048, "swish", "config5 batch-2048 d=8192 h=28672 n_m=8"),
 }
 DEFAULT_WORKLOAD = "decode_b1"
 METRIC = "SwiMGLU up-proj HBM GB/s at batch 1 (algorithmic W+codes+x+y bytes / time per call)"
+METRIC_TC = "SwiMGLU up-proj TFLOP/s at prefill (algorithmic 2*B*d*h*(n_m+1) flops / time per call)"
+PREFILL_MIN_B = 64          # workloads with more tokens are reported against the tensor roofline
 
 
 def algorithmic_bytes(d, h, n_m, B, elem=2):
     """W once, the packed codes once (n_m bits/element), x read, y written."""
     return h * d * elem + (h * d * n_m + 7) // 8 + B * d * elem + B * h * elem
+
+
+def algorithmic_flops(d, h, n_m, B):
+    """the (n_m + 1) GEMMs sharing x -- t and the n_m sign-flipped products."""
+    return 2 * B * d * h * (n_m + 1)
+
+
+def is_prefill(B):
+    return B >= PREFILL_MIN_B
+
+
+def work(d, h, n_m, B):
+    """(units per call, scale to the metric unit, unit, metric) of the workload's metric."""
+    if is_prefill(B):
+        return algorithmic_flops(d, h, n_m, B), 1e12, "TFLOP/s", METRIC_TC
+    return algorithmic_bytes(d, h, n_m, B), 1e9, "GB/s", METRIC
 
 
 def load_peaks():
@@ -207,16 +231,27 @@ def cublas_swiglu_us(d, h, B, L, K, stream):
     return res
 
 
+def oracle_sample_cols(d, h, n_m, B):
+    """Columns of the layer the oracle computes per pass: the whole layer for decode; for prefill
+    a bounded column sample (all B tokens, all d), so one pass stays around a second."""
+    if not is_prefill(B):
+        return h
+    per_col = 2 * B * d * (2 * n_m + 1)          # the oracle's own flops per output column
+    return int(max(1, min(h, 2e9 // per_col)))
+
+
 def cpu_baseline(d, h, n_m, B, act_code, budget_s=10.0):
     """The oracle as it stands (C, binary64, OpenMP over output columns) on the same workload:
-    full layer (all h columns, all d) per pass, passes repeated until ~budget_s of CPU work."""
+    full layer (decode) or a column sample (prefill) per pass, repeated until ~budget_s of CPU
+    work; the rate is scaled to the metric's unit from the columns actually computed."""
     from oracle import COracle
     o = COracle()
     rng = np.random.default_rng(0)
+    c = oracle_sample_cols(d, h, n_m, B)
     x = rng.standard_normal((B, d))
-    Wt = rng.uniform(-1 / d ** 0.5, 1 / d ** 0.5, (h, d))
+    Wt = rng.uniform(-1 / d ** 0.5, 1 / d ** 0.5, (c, d))
     packed = rng.integers(0, 256, (h * d * n_m + 7) // 8, dtype=np.uint8)
-    cols = np.arange(h)
+    cols = np.arange(c)
     passes, t0 = 0, time.perf_counter()
     while True:
         o.forward(x, Wt, cols, packed, n_m, act_code)
@@ -225,10 +260,11 @@ def cpu_baseline(d, h, n_m, B, act_code, budget_s=10.0):
         if el >= budget_s or passes >= 200:
             break
     per = el / passes
-    return {"value": algorithmic_bytes(d, h, n_m, B) / per / 1e9, "unit": "GB/s",
+    units, scale, unit, _ = work(d, c, n_m, B)
+    return {"value": units / per / scale, "unit": unit,
             "cores": o.num_threads(), "kind": "oracle",
-            "sample": f"full layer (B={B}, all {h} columns x {d}), {passes} passes in {el:.1f} s",
-            "seconds_per_call": per}
+            "sample": f"B={B} tokens x {c} of {h} columns x d={d} per pass, {passes} passes in {el:.1f} s",
+            "seconds_per_call": per * h / c}
 
 
 # ---------------------------------------------------------------- arms
@@ -241,10 +277,11 @@ def run_reference(args, ws, rank):
     d, h, n_m, B, act, desc = WORKLOADS[args.workload]
     o = COracle()
     rng = np.random.default_rng(0)
+    c = oracle_sample_cols(d, h, n_m, B)
     x = rng.standard_normal((B, d))
-    Wt = rng.uniform(-1 / d ** 0.5, 1 / d ** 0.5, (h, d))
+    Wt = rng.uniform(-1 / d ** 0.5, 1 / d ** 0.5, (c, d))
     packed = rng.integers(0, 256, (h * d * n_m + 7) // 8, dtype=np.uint8)
-    cols = np.arange(h)
+    cols = np.arange(c)
     for _ in range(args.warmup):
         o.forward(x, Wt, cols, packed, n_m, ACT_NAMES[act])
     t0 = time.perf_counter()
@@ -252,16 +289,18 @@ def run_reference(args, ws, rank):
         o.forward(x, Wt, cols, packed, n_m, ACT_NAMES[act])
     el = time.perf_counter() - t0
     per = el / args.steps
-    value = algorithmic_bytes(d, h, n_m, B) * args.steps / el / 1e9
+    units, scale, unit, metric = work(d, c, n_m, B)
+    value = units * args.steps / el / scale
+    sample = f"B={B} tokens x {c} of {h} columns x d={d} per step"
     return {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
+        "impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": desc, "d": d, "h": h, "n_m": n_m, "batch": B, "act": act},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": o.num_threads(), "kind": "oracle",
-                         "sample": f"full layer per step (B={B}, {h} columns x {d})"},
-        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": o.num_threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
@@ -310,12 +349,18 @@ def run_mglu(args, ws, rank, local):
         barrier(ws)
         sampler.stop()
     el_max = max_over_ranks(ws, el)
-    bytes_layer = algorithmic_bytes(d, h, n_m, B)
+    units_layer, scale, unit, metric = work(d, h, n_m, B)
+    units_rank = work(d, h_loc, n_m, B)[0]
     bytes_rank = algorithmic_bytes(d, h_loc, n_m, B)
-    value = bytes_layer * args.steps / el_max / 1e9
+    value = units_layer * args.steps / el_max / scale
     per_launch_s = el / args.steps / max(1, launches_per_step)
     peaks = load_peaks()
-    achieved = bytes_rank / per_launch_s / 1e9
+    achieved = units_rank / per_launch_s / scale
+    if is_prefill(B):
+        peak, peak_src = peaks["bf16_tflops_sustained"] or peaks["bf16_tflops"], "bf16_tflops_sustained (cuBLAS)"
+        bound = "tensor"
+    else:
+        peak, peak_src, bound = peaks["hbm_gbs"], "hbm_gbs (copy)", "hbm"
 
     # e2e through the C-ABI host-buffer entry: x H2D + kernel + y D2H every step
     xh = x.cpu().pin_memory()
@@ -333,7 +378,7 @@ def run_mglu(args, ws, rank, local):
         el_e2e = time_steps(step_host, args.steps, stream)
         barrier(ws)
     el_e2e = max_over_ranks(ws, el_e2e)
-    e2e = {"value": bytes_layer * args.steps / el_e2e / 1e9, "unit": "GB/s",
+    e2e = {"value": units_layer * args.steps / el_e2e / scale, "unit": unit,
            "h2d_bytes_per_step": B * d * 2 * ws, "d2h_bytes_per_step": B * h * 2,
            "us_per_call": el_e2e / args.steps * 1e6}
 
@@ -347,7 +392,7 @@ def run_mglu(args, ws, rank, local):
             if tr:
                 traffic = tr.get("dram_bytes_per_launch")
         out = {
-            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "metric": metric, "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": el_max / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (device-drawn, seeded: x~N(0,1), Wt~U(+-1/sqrt(d)), codes i.i.d. Bernoulli(0.5) bits)",
@@ -356,20 +401,21 @@ def run_mglu(args, ws, rank, local):
                        "l2": f"inputs larger than L2: {L} distinct layer copies ({L * bytes_rank / 1e6:.0f} MB/rank) rotated, no flush",
                        "kernel_path": path_used, "launch": "PDL (programmatic dependent launch) per call"},
             "us_per_call": el_max / args.steps * 1e6,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                         "peak_source": peaks["source"] + " hbm_gbs (copy)",
-                         "algorithmic_bytes_per_launch": bytes_rank},
+            "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peaks["source"] + " " + peak_src,
+                         "algorithmic_units_per_launch": units_rank, "algorithmic_bytes_per_launch": bytes_rank},
             "e2e": e2e,
             "gpu_launches": args.steps * launches_per_step,
             "clocks": sampler.summary(),
         }
         if not args.no_comparator and ws == 1:
-            cb = cublas_swiglu_us(d, h, B, L, args.steps, stream)
+            cb = cublas_swiglu_us(d, h, B, L, min(args.steps, 200 if not is_prefill(B) else 20), stream)
             out["cublas_swiglu"] = {"us_per_call": cb["best_us"], "two_gemm_us": cb["two_gemm"],
                                     "concat_gemm_us": cb["concat_gemm"],
                                     "mglu_speedup": cb["best_us"] / out["us_per_call"],
-                                    "bytes_per_call": 2 * h * d * 2 + B * d * 2 + B * h * 2}
+                                    "bytes_per_call": 2 * h * d * 2 + B * d * 2 + B * h * 2,
+                                    "tflops": 2 * B * d * 2 * h / (cb["best_us"] * 1e-6) / 1e12}
         if not args.no_cpu_baseline and ws == 1:
             from oracle import ACT_NAMES
             out["cpu_baseline"] = cpu_baseline(d, h, n_m, B, ACT_NAMES[act], budget_s=args.cpu_budget)

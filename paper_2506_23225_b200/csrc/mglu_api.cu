@@ -35,7 +35,6 @@ struct mglu_ctx {
   size_t x_stage_bytes = 0;
   void* y_stage = nullptr;
   size_t y_stage_bytes = 0;
-  mglu::TcState tc;
   // TMA descriptor cache of the decode path
   struct DecMaps {
     bool valid = false;
@@ -282,6 +281,75 @@ cudaError_t mma_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const voi
   }
 }
 
+// ------------------------------------------------------------------ tcgen05 (prefill) dispatch
+bool tc_can_serve(const mglu_ctx* hd, int64_t B) {
+  return hd->dtype == MGLU_BF16 && B >= 1 && B <= ((int64_t)1 << 31) - 1;
+}
+
+// 2-D row-major [rows][cols] bf16 tensor, box [brows][bcols]
+bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t bcols, uint32_t brows,
+                    CUtensorMapSwizzle swz) {
+  EncodeTiledFn enc = get_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {bcols, brows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NM, int ACT>
+cudaError_t run_tc(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
+                   cudaStream_t st) {
+  constexpr int BN = mglu::tc_bn<NM>(), BK = mglu::tc_bk<NM>();
+  CUtensorMap mW, mX;
+  const auto swz = swizzle_for(2 * BK);
+  if (!encode_2d_bf16(&mW, Wt, hd->d, hd->h, BK, 128, swz) || !encode_2d_bf16(&mX, x, hd->d, B, BK, BN, swz))
+    return cudaErrorInvalidValue;
+  mglu::TcParams p;
+  p.codes = (const uint32_t*)codes;
+  p.out = (__nv_bfloat16*)out;
+  p.B = (int)B;
+  p.d = (int)hd->d;
+  p.h = (int)hd->h;
+  constexpr size_t SB = mglu::tc_stage_bytes<NM>();
+  const size_t fixed = 1024 + 256;           // alignment slack + barriers / TMEM slot
+  const size_t cap = (size_t)hd->max_smem_optin;
+  if (cap < fixed + 2 * SB) return cudaErrorInvalidConfiguration;
+  int S = (int)std::min<size_t>(4, (cap - fixed) / SB);
+  p.stages = S;
+  const size_t smem = (size_t)S * SB + fixed;
+  auto kern = mglu::gemm_tc_kernel<NM, ACT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const dim3 grid((unsigned)((B + BN - 1) / BN), (unsigned)((hd->h + 127) / 128));
+  return launch_pdl(kern, grid, dim3(mglu::kTcThreads), smem, st, p, mW, mX);
+}
+
+template <int NM>
+cudaError_t tc_act(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
+                   cudaStream_t st) {
+  switch (hd->act) {
+    case MGLU_ACT_IDENTITY: return run_tc<NM, mglu::kIdentity>(hd, x, B, Wt, codes, out, st);
+    case MGLU_ACT_SWISH: return run_tc<NM, mglu::kSwish>(hd, x, B, Wt, codes, out, st);
+    case MGLU_ACT_GELU: return run_tc<NM, mglu::kGelu>(hd, x, B, Wt, codes, out, st);
+    case MGLU_ACT_RELU: return run_tc<NM, mglu::kRelu>(hd, x, B, Wt, codes, out, st);
+    default: return run_tc<NM, mglu::kSigmoid>(hd, x, B, Wt, codes, out, st);
+  }
+}
+
+cudaError_t tc_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
+                  cudaStream_t st) {
+  switch (hd->n_m) {
+    case 1: return tc_act<1>(hd, x, B, Wt, codes, out, st);
+    case 2: return tc_act<2>(hd, x, B, Wt, codes, out, st);
+    case 4: return tc_act<4>(hd, x, B, Wt, codes, out, st);
+    default: return tc_act<8>(hd, x, B, Wt, codes, out, st);
+  }
+}
+
 mglu_status check_ptrs(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes,
                        const void* out) {
   if (!hd) return MGLU_ERR_INVALID_ARG;
@@ -374,7 +442,6 @@ mglu_status mglu_destroy(mglu_handle hd) {
   cudaSetDevice(hd->device);
   if (hd->x_stage) cudaFree(hd->x_stage);
   if (hd->y_stage) cudaFree(hd->y_stage);
-  mglu::tc_release(hd->tc);
   cudaSetDevice(prev);
   delete hd;
   return MGLU_OK;
@@ -402,10 +469,10 @@ mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* W
     path = hd->path;
   }
   if (path == MGLU_PATH_AUTO) {
-    if (hd->dtype == MGLU_BF16 && mglu::tc_can_serve(hd->d, hd->h, hd->n_m, B) && B > 64)
-      path = MGLU_PATH_TCGEN05;
-    else if (mma_can_serve(hd, B))
+    if (mma_can_serve(hd, B))
       path = MGLU_PATH_MMA;
+    else if (tc_can_serve(hd, B))
+      path = MGLU_PATH_TCGEN05;
     else
       path = MGLU_PATH_SIMT;
   }
@@ -423,11 +490,12 @@ mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* W
     e = mma_nm(hd, x, (int)B, Wt, packed, out, st);
     launches = 1;
   } else if (path == MGLU_PATH_TCGEN05) {
-    if (hd->dtype != MGLU_BF16 || !mglu::tc_can_serve(hd->d, hd->h, hd->n_m, B)) {
+    if (!tc_can_serve(hd, B)) {
       if (prev != hd->device) cudaSetDevice(prev);
-      return set_err(hd, MGLU_ERR_UNSUPPORTED, "tcgen05 path needs bf16, d % 64 == 0, h % 128 == 0");
+      return set_err(hd, MGLU_ERR_UNSUPPORTED, "tcgen05 path needs bf16");
     }
-    e = mglu::tc_forward(hd->tc, hd->d, hd->h, hd->n_m, hd->act, x, B, Wt, packed, out, st, &launches);
+    e = tc_nm(hd, x, B, Wt, packed, out, st);
+    launches = 1;
   } else {
     e = hd->dtype == MGLU_BF16
             ? simt_nm<__nv_bfloat16, false>(hd, x, (int)B, Wt, packed, out, nullptr, st)
