@@ -1,20 +1,24 @@
-// gemm_tc.cuh -- tcgen05/TMEM masked GEMM: the prefill / large-batch regime (a8).  MGLU_PATH_TCGEN05.
+// gemm_tc.cuh -- tcgen05/TMEM masked GEMM: the prefill / large-batch regime.
 //
-// The paper's kernel is batch 1 only; for B tokens Eq. 3 needs (n_m + 1) GEMMs that share
-// x: t = X Wt^T and, per mask, the gated product.  As in the decode regime the masked operand is
-// the sign-flipped weight sigma_i (.) W (sigma = +1 on the gate side, -1 on the value side), so
-// the tensor core accumulates u_i = s_i - v_i and the epilogue uses s_i = (t + u_i) / 2.
+// The paper's kernel is batch 1 only; for B tokens Eq. 3 needs (n_m + 1) GEMMs sharing x:
+// t = X Wt^T and, per mask, a masked product.  As in the decode regime the masked operand is the
+// sign-flipped weight sigma_i (.) W (sigma = +1 where M_i = 1, -1 where M_i = 0), so the tensor core
+// accumulates u_i = s_i - v_i and the epilogue takes s_i = (t + u_i) / 2 (exact rescaling).
 //
-// One CTA computes a 128-row (h) x BN-token tile.  Warp roles (192 threads):
-//   warp 4   TMA producer: W tile [128 x BK] and x tile [BN x BK] (K-major, swizzled) per stage;
-//   warps 0-3 masker: thread m reads its row of the W tile, builds the n_m sign-flipped rows from
-//            the row's mask words (one IMAD + one LOP3 per bf16 pair and mask) and stores them in
-//            the same swizzled K-major layout (the masked operands live in shared memory);
-//   warp 5   MMA issuer (one thread): per k16 step, (n_m + 1) tcgen05.mma kind::f16 into
-//            (n_m + 1) TMEM accumulators of BN fp32 columns each; tcgen05.commit frees the stage;
-//   warps 0-3 epilogue: tcgen05.ld of row m's accumulators (TMEM lane m), Eq. 3 on registers,
-//            bf16 stores y[token][row] (32 consecutive rows per warp store = coalesced).
-// TMEM: (n_m + 1) * BN <= 512 columns fixes BN = 256 / 128 / 64 / 32 for n_m = 1 / 2 / 4 / 8.
+// One CTA computes a 128-row (h) x BN-token tile over the whole reduction (d).  Operands:
+//   * A = the n_m + 1 weight operands {W, sigma_1 (.) W, ...} live in TENSOR MEMORY (TS form): the
+//     masker warps read W rows straight from global memory (whole 32-byte sectors per thread),
+//     build the sign-flipped rows in registers (one IMAD + one LOP3 per bf16 pair and mask) and
+//     tcgen05.st them into a ring of SA TMEM A slots of KA columns of K each.  Shared memory
+//     carries only x, so the tensor core is not starved by shared-memory bandwidth (an
+//     SS form at N <= 128 needs > 128 B/clk of operand reads).
+//   * B = the x tile [BN tokens x 64] (K-major, 128-byte swizzle) staged by TMA in a shared ring.
+//   * D = n_m + 1 fp32 accumulators of BN columns each in TMEM:
+//     (n_m + 1) * BN + SA * (n_m + 1) * KA / 2 <= 512 columns.
+// Warp roles (320 threads): warps 0-7 masker (group g = warp / 4 fills the A slots of the A-stages
+// js = g mod 2; warp w owns TMEM lanes 32 (w % 4) .. +31 = tile rows), then epilogue (tcgen05.ld,
+// Eq. 3 in registers, bf16 stores; group g takes half the tokens); warp 8 TMA producer; warp 9 MMA
+// issuer (warp-uniform loop, one elected lane issues; one a_full wait and one commit per A-stage).
 #pragma once
 #include "common.cuh"
 #include "mma_mask.cuh"
@@ -23,183 +27,242 @@
 
 namespace mglu {
 
-template <int NM> __host__ __device__ constexpr int tc_bn() { return NM == 1 ? 256 : NM == 2 ? 128 : NM == 4 ? 64 : 32; }
-template <int NM> __host__ __device__ constexpr int tc_bk() { return NM == 8 ? 32 : 64; }
-template <int NM> __host__ __device__ constexpr int tc_tmem_cols() {
-  return (NM + 1) * tc_bn<NM>() <= 256 ? 256 : 512;
+// tile shape per mask count: BN tokens; SA TMEM A slots of KA reduction columns per operand
+template <int NM> struct TcCfg;
+template <> struct TcCfg<1> { static constexpr int BN = 224, SA = 2, KA = 32; };
+template <> struct TcCfg<2> { static constexpr int BN = 128, SA = 2, KA = 32; };
+template <> struct TcCfg<4> { static constexpr int BN = 64, SA = 2, KA = 32; };
+template <> struct TcCfg<8> { static constexpr int BN = 32, SA = 2, KA = 16; };
+
+constexpr int kTcThreads = 320;
+constexpr int kTcMaskWarps = 8;
+constexpr int kTcXK = 64;                       // K per x stage (128-byte rows)
+constexpr int kTcPrefetch = 2;                  // masker register prefetch depth (A-stages of its group)
+
+template <int NM> __host__ __device__ constexpr int tc_x_stage_bytes() { return TcCfg<NM>::BN * kTcXK * 2; }
+template <int NM> __host__ __device__ constexpr int tc_tmem_used() {
+  return (NM + 1) * TcCfg<NM>::BN + TcCfg<NM>::SA * (NM + 1) * TcCfg<NM>::KA / 2;
 }
-template <int NM> __host__ __device__ constexpr int tc_stage_bytes() {
-  // W tile + x tile + n_m masked tiles, all [rows][BK] bf16
-  return 128 * tc_bk<NM>() * 2 + tc_bn<NM>() * tc_bk<NM>() * 2 + NM * 128 * tc_bk<NM>() * 2;
+static_assert(tc_tmem_used<1>() <= 512 && tc_tmem_used<2>() <= 512 && tc_tmem_used<4>() <= 512 &&
+              tc_tmem_used<8>() <= 512, "TMEM budget");
+
+// the n_m code words of one (row, 32-column group), vector loads, L1-allocating
+template <int NM> __device__ __forceinline__ void ld_words(const uint32_t* p, uint32_t (&c)[NM]) {
+  if constexpr (NM == 1) {
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(c[0]) : "l"(p));
+  } else if constexpr (NM == 2) {
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(c[0]), "=r"(c[1]) : "l"(p));
+  } else if constexpr (NM == 4) {
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]) : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]), "=r"(c[7])
+                 : "l"(p));
+  }
 }
-constexpr int kTcThreads = 192;
 
 struct TcParams {
+  const __nv_bfloat16* Wt;   // [h][d]
   const uint32_t* codes;     // packed mask words (R3 layout)
   __nv_bfloat16* out;        // [B][h]
   int B, d, h;
-  int stages;
+  int xstages;
 };
+
+// Masker group G (0/1) builds the A operands of the A-stages js = G, G + 2, ... (KA columns each)
+// for the tile row this thread owns (TMEM lane): W straight from global memory (KA * 2 bytes =
+// whole sectors), the row's n_m code words of the 32-column group, n_m sign flips per bf16 pair,
+// n_m + 1 tcgen05.st.  A-stage js uses slot js % SA (SA even): each slot belongs to one group,
+// which visits its slots in order, so the parity waits can never skip a phase.
+template <int NM, int G>
+__device__ __forceinline__ void tc_masker(const __nv_bfloat16* wrow, const uint32_t* crow, int nstages,
+                                          uint32_t a_lane, uint64_t* a_full, uint64_t* a_empty) {
+  constexpr int SA = TcCfg<NM>::SA, KA = TcCfg<NM>::KA;
+  constexpr int NOP = NM + 1, WW = KA / 2;                 // u32 words (bf16 pairs) per row and stage
+  static_assert(SA % 2 == 0, "A slots must split evenly between the two masker groups");
+  static_assert(KA == 32 || KA == 16, "A-stage width");
+  constexpr int PAIR0 = KA == 32 ? 0 : 8 * G;              // first pair of the stage in its code group
+  uint32_t wb[kTcPrefetch][WW], cb[kTcPrefetch][NM];
+  auto fetch = [&](int js, uint32_t (&w)[WW], uint32_t (&c)[NM]) {
+    if (js < nstages) {
+      ld_nc_v8_na(wrow + KA * js, *reinterpret_cast<uint32_t(*)[8]>(&w[0]));
+      if constexpr (WW == 16) ld_nc_v8_na(wrow + KA * js + 16, *reinterpret_cast<uint32_t(*)[8]>(&w[8]));
+      ld_words<NM>(crow + (size_t)((KA * js) >> 5) * NM, c);
+    }
+  };
+#pragma unroll
+  for (int u = 0; u < kTcPrefetch; ++u) fetch(G + 2 * u, wb[u], cb[u]);
+  for (int js0 = G; js0 < nstages; js0 += 2 * kTcPrefetch) {
+#pragma unroll
+    for (int u = 0; u < kTcPrefetch; ++u) {
+      const int js = js0 + 2 * u;
+      if (js < nstages) {
+        uint32_t a[NOP][WW];
+#pragma unroll
+        for (int q = 0; q < WW; ++q) a[0][q] = wb[u][q];
+#pragma unroll
+        for (int i = 0; i < NM; ++i) {
+#pragma unroll
+          for (int q = 0; q < WW; ++q)                     // pair PAIR0 + q: bits (pair, pair + 16)
+            a[1 + i][q] = sign_flip(wb[u][q], cb[u][i], 1u << (15 - PAIR0 - q));
+        }
+        fetch(js + 2 * kTcPrefetch, wb[u], cb[u]);         // refill this buffer
+        const int sa = js % SA;
+        mbar_wait(&a_empty[sa], ((uint32_t)(js / SA) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t a0 = a_lane + (uint32_t)(sa * NOP * WW);
+#pragma unroll
+        for (int op = 0; op < NOP; ++op) {
+          if constexpr (WW == 16) tmem_st16(a0 + op * WW, a[op]);
+          else tmem_st8(a0 + op * WW, *reinterpret_cast<uint32_t(*)[8]>(&a[op][0]));
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&a_full[sa]);
+      }
+    }
+  }
+}
 
 template <int NM, int ACT>
 __global__ void __launch_bounds__(kTcThreads, 1)
-gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mW, const __grid_constant__ CUtensorMap mX) {
-  constexpr int BN = tc_bn<NM>(), BK = tc_bk<NM>();
-  constexpr int SPAN = BK * 2;                         // bytes per tile row (= swizzle span)
-  constexpr int WT = 128 * SPAN, XT = BN * SPAN;       // tile bytes
-  constexpr int SB = tc_stage_bytes<NM>();
-  constexpr int GPK = BK / 32;                         // 32-column mask groups per k-block
+gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX) {
+  constexpr int BN = TcCfg<NM>::BN, SA = TcCfg<NM>::SA, KA = TcCfg<NM>::KA;
+  constexpr int NOP = NM + 1;                              // operands: W and n_m sign-flipped copies
+  constexpr int XB = tc_x_stage_bytes<NM>();
+  constexpr int KPS = KA / 16;                             // k16 steps per A-stage
   constexpr uint32_t IDESC = idesc_bf16_f32(128, BN);
-  constexpr int TMEM_COLS = tc_tmem_cols<NM>();
+  constexpr uint32_t A_COL0 = NOP * BN;                    // first TMEM column of the A ring
+  static_assert((kTcXK / 16) % (KPS * SA) == 0, "the slot pattern repeats within an x stage");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // swizzle atoms (and the descriptors' base offset 0) need 1024-byte aligned tiles
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int S = p.stages;
-  uint8_t* ring = smem;                                // per stage: W | x | masked[NM]
-  uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB);
-  uint64_t* mask_full = tma_full + S;
-  uint64_t* empty = mask_full + S;
-  uint64_t* acc_full = empty + S;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  const int SX = p.xstages;
+  uint8_t* xring = smem;
+  uint64_t* x_full = reinterpret_cast<uint64_t*>(smem + (size_t)SX * XB);
+  uint64_t* x_empty = x_full + SX;
+  uint64_t* a_full = x_empty + SX;
+  uint64_t* a_empty = a_full + SA;
+  uint64_t* acc_full = a_empty + SA;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * 128;
   const int d = p.d;
-  const int nkb = (d + BK - 1) / BK;
+  const int nk16 = d >> 4;                                 // d % 32 == 0
+  const int nkx = (d + kTcXK - 1) / kTcXK;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&tma_full[s], 1);
-      mbar_init(&mask_full[s], 128);
-      mbar_init(&empty[s], 1);
-    }
+    for (int s = 0; s < SX; ++s) { mbar_init(&x_full[s], 1); mbar_init(&x_empty[s], 1); }
+    for (int s = 0; s < SA; ++s) { mbar_init(&a_full[s], 128); mbar_init(&a_empty[s], 1); }
     mbar_init(acc_full, 1);
     mbar_fence_init();
   }
-  if (warp == 0) tmem_alloc(tmem_base_slot, TMEM_COLS);
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_base_slot;
+  const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
-    // ---------------------------------------------------------------- TMA producer
+  if (warp == kTcMaskWarps) {
+    // ---------------------------------------------------------------- TMA producer (x)
     if (lane == 0) {
-      prefetch_tmap(&mW);
       prefetch_tmap(&mX);
-      pdl_wait();                                                  // x may come from the predecessor
+      pdl_wait();                                          // x may come from the predecessor
       int s = 0;
       uint32_t ph = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* st = ring + (size_t)s * SB;
-        mbar_arrive_expect_tx(&tma_full[s], (uint32_t)(WT + XT));
-        tma_load_2d(st, &mW, kb * BK, m0, &tma_full[s]);
-        tma_load_2d(st + WT, &mX, kb * BK, n0, &tma_full[s]);
-        if (++s == S) { s = 0; ph ^= 1; }
+      for (int kx = 0; kx < nkx; ++kx) {
+        mbar_wait(&x_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&x_full[s], (uint32_t)XB);
+        tma_load_2d(xring + (size_t)s * XB, &mX, kx * kTcXK, n0, &x_full[s]);
+        if (++s == SX) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp == 5) {
-    // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&mask_full[s], ph);
-        tc_fence_after();
-        const uint32_t base = smem_u32(ring + (size_t)s * SB);
+  } else if (warp == kTcMaskWarps + 1) {
+    // ---------------------------------------------------------------- MMA issuer (whole warp)
+    const uint64_t bdesc0 = smem_desc_kmajor(smem_u32(xring), 128);
+    int sx = 0;
+    uint32_t phx = 0;
+    for (int kx = 0; kx < nkx; ++kx) {
+      mbar_wait(&x_full[sx], phx);
+      tc_fence_after();
+      const uint64_t bdesc_s = bdesc0 + (uint64_t)((sx * XB) >> 4);
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint32_t koff = kk * 32;                           // 16 bf16 along K
-          const uint64_t bdesc = smem_desc_kmajor(base + WT + koff, SPAN);
-          const uint32_t acc = (kb | kk) ? 1u : 0u;
-          tc_mma_ss(tmem, smem_desc_kmajor(base + koff, SPAN), bdesc, IDESC, acc);      // t
+      for (int kk = 0; kk < kTcXK / 16; ++kk) {
+        const int j = kx * (kTcXK / 16) + kk;              // k16 step
+        if (j < nk16) {
+          const int js = j / KPS;                          // A-stage
+          const int sa = (kk / KPS) % SA;                  // == js % SA (x stages hold whole slot cycles)
+          if (kk % KPS == 0) {
+            mbar_wait(&a_full[sa], (uint32_t)(js / SA) & 1u);
+            tc_fence_after();
+          }
+          if (elect_one()) {
+            const uint64_t bdesc = bdesc_s + (uint64_t)(kk * 2);          // +32 bytes along K
+            const uint32_t a0 = tmem + A_COL0 + (uint32_t)(sa * NOP * (KA / 2) + (kk % KPS) * 8);
+            const uint32_t acc = j > 0 ? 1u : 0u;
 #pragma unroll
-          for (int i = 0; i < NM; ++i)                                                  // u_i
-            tc_mma_ss(tmem + (1 + i) * BN, smem_desc_kmajor(base + WT + XT + i * WT + koff, SPAN), bdesc,
-                      IDESC, acc);
+            for (int op = 0; op < NOP; ++op)
+              tc_mma_ts(tmem + op * BN, a0 + op * (KA / 2), bdesc, IDESC, acc);
+            if (kk % KPS == KPS - 1) tc_commit(&a_empty[sa]);
+          }
+          __syncwarp();
         }
-        tc_commit(&empty[s]);                                      // frees the stage when done
-        if (++s == S) { s = 0; ph ^= 1; }
       }
-      tc_commit(acc_full);
+      if (elect_one()) tc_commit(&x_empty[sx]);
+      __syncwarp();
+      if (++sx == SX) { sx = 0; phx ^= 1; }
     }
+    if (elect_one()) tc_commit(acc_full);
+    __syncwarp();
   } else {
-    // ---------------------------------------------------------------- masker (then epilogue)
-    const int m = threadIdx.x;                                     // tile row 0..127
+    // ---------------------------------------------------------------- masker
+    const int g = warp >> 2;
+    const int m = (warp & 3) * 32 + lane;                  // tile row = TMEM lane
     const int grow = m0 + m;
-    const int mrow = grow < p.h ? grow : p.h - 1;                  // rows past h: any valid row
-    const uint32_t* crow = p.codes + (size_t)mrow * (d / 32) * NM;
-    const uint32_t row_off = (uint32_t)((m >> 3) * (8 * SPAN) + (m & 7) * SPAN);
-    uint32_t cw[GPK * NM], cn[GPK * NM];
-#pragma unroll
-    for (int q = 0; q < GPK * NM; ++q) cn[q] = ((q / NM) * 32 < d) ? ld_nc_u32(crow + q) : 0u;
-    int s = 0;
-    uint32_t ph = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
-#pragma unroll
-      for (int q = 0; q < GPK * NM; ++q) cw[q] = cn[q];
-      if (kb + 1 < nkb) {                                          // prefetch the next block's words
-        const int g_next = (kb + 1) * GPK;
-#pragma unroll
-        for (int q = 0; q < GPK * NM; ++q)
-          cn[q] = (g_next * 32 + (q / NM) * 32 < d) ? ld_nc_u32(crow + (size_t)g_next * NM + q) : 0u;
-      }
-      mbar_wait(&empty[s], ph ^ 1);                                // MMA done with this slot
-      mbar_wait(&tma_full[s], ph);                                 // W tile landed
-      uint8_t* st = ring + (size_t)s * SB;
-#pragma unroll
-      for (int c = 0; c < BK / 8; ++c) {                           // 16-byte chunks of the row
-        // TMA / UMMA swizzle: 16-byte chunk bits [4, 4+log2(SPAN/16)) ^= address bits [7, ...)
-        const uint32_t lin = row_off + (uint32_t)c * 16;
-        const uint32_t off = lin ^ (((lin >> 7) & (uint32_t)(SPAN / 16 - 1)) << 4);
-        const uint4 w = *reinterpret_cast<const uint4*>(st + off);
-        const int g = c >> 2, qb = 4 * (c & 3);                    // group, first pair's bit
-#pragma unroll
-        for (int i = 0; i < NM; ++i) {
-          const uint32_t word = cw[g * NM + i];
-          uint4 o;
-          o.x = sign_flip(w.x, word, 1u << (15 - qb));
-          o.y = sign_flip(w.y, word, 1u << (14 - qb));
-          o.z = sign_flip(w.z, word, 1u << (13 - qb));
-          o.w = sign_flip(w.w, word, 1u << (12 - qb));
-          *reinterpret_cast<uint4*>(st + WT + XT + i * WT + off) = o;
-        }
-      }
-      fence_async_smem();
-      mbar_arrive(&mask_full[s]);
-      if (++s == S) { s = 0; ph ^= 1; }
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    {
+      const int mrow = grow < p.h ? grow : p.h - 1;        // rows past h: any valid row, discarded
+      const __nv_bfloat16* wrow = p.Wt + (size_t)mrow * d;
+      const uint32_t* crow = p.codes + (size_t)mrow * (d / 32) * NM;
+      const uint32_t a_lane = tmem + lane_off + A_COL0;
+      const int nstages = d / KA;
+      if (g == 0)
+        tc_masker<NM, 0>(wrow, crow, nstages, a_lane, a_full, a_empty);
+      else
+        tc_masker<NM, 1>(wrow, crow, nstages, a_lane, a_full, a_empty);
     }
 
     // ---------------------------------------------------------------- epilogue
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    pdl_wait();                                                    // out may be read upstream
-    const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
+    pdl_wait();                                            // out may be read upstream
+    const uint32_t lane_base = tmem + lane_off;
+    constexpr int HALF = BN / 2;                           // tokens per masker group
+    static_assert(HALF % 8 == 0, "BN / 2 must be a multiple of 8");
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t tv[16], uv[16];
-      float y[16];
-      tmem_ld16(lane_base + c0, tv);
+    for (int c0 = g * HALF; c0 < (g + 1) * HALF; c0 += 8) {
+      uint32_t tv[8], uv[8];
+      float y[8];
+      tmem_ld8(lane_base + c0, tv);
       tmem_ld_wait();
 #pragma unroll
-      for (int j = 0; j < 16; ++j) y[j] = 0.f;
-#pragma unroll 1
+      for (int q = 0; q < 8; ++q) y[q] = 0.f;
+#pragma unroll
       for (int i = 0; i < NM; ++i) {
-        tmem_ld16(lane_base + (1 + i) * BN + c0, uv);
+        tmem_ld8(lane_base + (1 + i) * BN + c0, uv);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float t = __uint_as_float(tv[j]);
-          const float sgate = 0.5f * (t + __uint_as_float(uv[j]));          // s_i = (t + u_i) / 2
-          y[j] = fmaf(act_g<ACT>(sgate), t - sgate, y[j]);                 // g(s_i) (t - s_i)
+        for (int q = 0; q < 8; ++q) {
+          const float t = __uint_as_float(tv[q]);
+          const float sg = 0.5f * (t + __uint_as_float(uv[q]));           // s_i = (t + u_i) / 2
+          y[q] = fmaf(act_g<ACT>(sg), t - sg, y[q]);                      // g(s_i) (t - s_i)
         }
       }
       if (grow < p.h) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int tok = n0 + c0 + j;
-          if (tok < p.B) p.out[(size_t)tok * p.h + grow] = __float2bfloat16_rn(y[j]);
+        for (int q = 0; q < 8; ++q) {
+          const int tok = n0 + c0 + q;
+          if (tok < p.B) p.out[(size_t)tok * p.h + grow] = __float2bfloat16_rn(y[q]);
         }
       }
     }
@@ -207,7 +270,7 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mW, const _
   tc_fence_before();
   __syncthreads();
   pdl_launch_dependents();
-  if (warp == 0) tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
 }  // namespace mglu

@@ -303,29 +303,25 @@ bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t ro
 template <int NM, int ACT>
 cudaError_t run_tc(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
                    cudaStream_t st) {
-  constexpr int BN = mglu::tc_bn<NM>(), BK = mglu::tc_bk<NM>();
-  CUtensorMap mW, mX;
-  const auto swz = swizzle_for(2 * BK);
-  if (!encode_2d_bf16(&mW, Wt, hd->d, hd->h, BK, 128, swz) || !encode_2d_bf16(&mX, x, hd->d, B, BK, BN, swz))
-    return cudaErrorInvalidValue;
+  constexpr int BN = mglu::TcCfg<NM>::BN;
+  CUtensorMap mX;
+  if (!encode_2d_bf16(&mX, x, hd->d, B, mglu::kTcXK, BN, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
   mglu::TcParams p;
+  p.Wt = (const __nv_bfloat16*)Wt;
   p.codes = (const uint32_t*)codes;
   p.out = (__nv_bfloat16*)out;
   p.B = (int)B;
   p.d = (int)hd->d;
   p.h = (int)hd->h;
-  constexpr size_t SB = mglu::tc_stage_bytes<NM>();
-  const size_t fixed = 1024 + 256;           // alignment slack + barriers / TMEM slot
-  const size_t cap = (size_t)hd->max_smem_optin;
-  if (cap < fixed + 2 * SB) return cudaErrorInvalidConfiguration;
-  int S = (int)std::min<size_t>(4, (cap - fixed) / SB);
-  p.stages = S;
-  const size_t smem = (size_t)S * SB + fixed;
+  constexpr size_t XB = mglu::tc_x_stage_bytes<NM>();
+  const int SX = 6;
+  p.xstages = SX;
+  const size_t smem = (size_t)SX * XB + 1024 + 256;     // ring + alignment slack + barriers
   auto kern = mglu::gemm_tc_kernel<NM, ACT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const dim3 grid((unsigned)((B + BN - 1) / BN), (unsigned)((hd->h + 127) / 128));
-  return launch_pdl(kern, grid, dim3(mglu::kTcThreads), smem, st, p, mW, mX);
+  return launch_pdl(kern, grid, dim3(mglu::kTcThreads), smem, st, p, mX);
 }
 
 template <int NM>
