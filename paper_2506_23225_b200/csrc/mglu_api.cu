@@ -283,7 +283,8 @@ cudaError_t mma_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const voi
 
 // ------------------------------------------------------------------ tcgen05 (prefill) dispatch
 bool tc_can_serve(const mglu_ctx* hd, int64_t B) {
-  return hd->dtype == MGLU_BF16 && B >= 1 && B <= ((int64_t)1 << 31) - 1;
+  // TMA of the mask words: rows of d/32 * n_m u32 words must be 16-byte multiples
+  return hd->dtype == MGLU_BF16 && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 && B <= ((int64_t)1 << 31) - 1;
 }
 
 // 2-D row-major [rows][cols] bf16 tensor, box [brows][bcols]
@@ -300,28 +301,46 @@ bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t ro
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 2-D row-major [rows][cols] u32 tensor, box [brows][bcols], no swizzle
+bool encode_2d_u32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t bcols, uint32_t brows) {
+  EncodeTiledFn enc = get_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 4};
+  cuuint32_t box[2] = {bcols, brows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int NM, int ACT>
 cudaError_t run_tc(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
                    cudaStream_t st) {
   constexpr int BN = mglu::TcCfg<NM>::BN;
-  CUtensorMap mX;
-  if (!encode_2d_bf16(&mX, x, hd->d, B, mglu::kTcXK, BN, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  CUtensorMap mX, mW, mC;
+  const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
+  if (!encode_2d_bf16(&mX, x, hd->d, B, mglu::kTcK, BN, sw) ||
+      !encode_2d_bf16(&mW, Wt, hd->d, hd->h, mglu::kTcK, 128, sw) ||
+      !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, mglu::tc_code_words<NM>(), 128))
+    return cudaErrorInvalidValue;
   mglu::TcParams p;
-  p.Wt = (const __nv_bfloat16*)Wt;
-  p.codes = (const uint32_t*)codes;
   p.out = (__nv_bfloat16*)out;
   p.B = (int)B;
   p.d = (int)hd->d;
   p.h = (int)hd->h;
-  constexpr size_t XB = mglu::tc_x_stage_bytes<NM>();
-  const int SX = 6;
-  p.xstages = SX;
-  const size_t smem = (size_t)SX * XB + 1024 + 256;     // ring + alignment slack + barriers
+  constexpr size_t SB = mglu::tc_stage_bytes<NM>();
+  const size_t fixed = 1024 + 256;                          // alignment slack + barriers / TMEM slot
+  const size_t cap = (size_t)hd->max_smem_optin;
+  if (cap < fixed + 2 * SB) return cudaErrorInvalidConfiguration;
+  const int S = (int)std::min<size_t>(6, (cap - fixed) / SB);
+  p.stages = S;
+  const size_t smem = (size_t)S * SB + fixed;
   auto kern = mglu::gemm_tc_kernel<NM, ACT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const dim3 grid((unsigned)((B + BN - 1) / BN), (unsigned)((hd->h + 127) / 128));
-  return launch_pdl(kern, grid, dim3(mglu::kTcThreads), smem, st, p, mX);
+  return launch_pdl(kern, grid, dim3(mglu::kTcThreads), smem, st, p, mX, mW, mC);
 }
 
 template <int NM>
@@ -488,7 +507,7 @@ mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* W
   } else if (path == MGLU_PATH_TCGEN05) {
     if (!tc_can_serve(hd, B)) {
       if (prev != hd->device) cudaSetDevice(prev);
-      return set_err(hd, MGLU_ERR_UNSUPPORTED, "tcgen05 path needs bf16");
+      return set_err(hd, MGLU_ERR_UNSUPPORTED, "tcgen05 path needs bf16 and d * n_m % 128 == 0");
     }
     e = tc_nm(hd, x, B, Wt, packed, out, st);
     launches = 1;

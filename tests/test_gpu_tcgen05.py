@@ -1,8 +1,9 @@
 """GPU parity of the tcgen05/TMEM masked GEMM (the prefill / large-batch regime)
 against the CPU oracle on identical seeded inputs.
 
-Shapes span several 128-row M tiles and BN-token N tiles (BN = 256/128/64/32 for n_m = 1/2/4/8)
-with ragged tails in every dimension, including a final half K-block (d % 64 == 32)."""
+Shapes span several 128-row M tiles and BN-token N tiles (BN = 224/128/64/32 for n_m = 1/2/4/8)
+with ragged tails in every dimension, including a final half K-block (d % 64 == 32); shapes whose
+mask-word rows are not 16-byte multiples (d * n_m % 128 != 0) must be refused as UNSUPPORTED."""
 import numpy as np
 import pytest
 import torch
@@ -22,7 +23,7 @@ def _lib():
 
 TC_SHAPES = [  # (d, h, B)
     (64, 128, 1), (128, 200, 65), (96, 130, 17), (256, 333, 130), (1024, 256, 300), (4096, 384, 257),
-    (2080, 129, 40),
+    (2080, 129, 40), (2112, 140, 230), (192, 64, 480),
 ]
 
 
@@ -30,6 +31,13 @@ TC_SHAPES = [  # (d, h, B)
 @pytest.mark.parametrize("d,h,B", TC_SHAPES)
 def test_tc_shapes(n_m, d, h, B):
     inp = make_inputs(5000 + 13 * n_m + d + h + B, B=B, d=d, h=h, n_m=n_m, dtype="bf16")
+    if (d // 32 * n_m) % 4:
+        # the mask-word rows are fetched by TMA: d * n_m must be a multiple of 128
+        from paper_2506_23225_b200.mglu import MgluError, MGLU_ERR_UNSUPPORTED
+        with pytest.raises(MgluError) as e:
+            gpu_forward(inp, "bf16", n_m, "swish", path="tcgen05")
+        assert e.value.status == MGLU_ERR_UNSUPPORTED
+        return
     y, used = gpu_forward(inp, "bf16", n_m, "swish", path="tcgen05")
     assert used == "tcgen05"
     ref = oracle_forward(inp, "bf16", n_m, "swish")
@@ -50,7 +58,7 @@ def test_tc_one_hot_bit_exact(n_m):
     every accumulator is a small integer, so y[k][j] = (n_m - popcount(c[j,k])) / 2 exactly --
     the mask decode of every (row, column) checked bit-exactly through the tensor-core path."""
     from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
-    d, h = 320, 200
+    d, h = 384, 200
     inp = make_inputs(61 + n_m, B=1, d=d, h=h, n_m=n_m, dtype="bf16")
     bits = inp["bits"]
     packed = torch.from_numpy(mglu_pack_masks_host(bits)).cuda()
