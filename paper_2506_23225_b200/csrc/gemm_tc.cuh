@@ -79,7 +79,8 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
   uint64_t* acc_full = a_empty + SA;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);   // provably warp-uniform
+  const int lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * 128;
   const int d = p.d;
   const int nk16 = d >> 4;                                 // d % 32 == 0
