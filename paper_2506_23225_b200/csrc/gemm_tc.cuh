@@ -25,12 +25,14 @@
 
 namespace mglu {
 
-// tile shape per mask count: BN tokens; 2 TMEM A slots of KA reduction columns per operand
+// tile shape per mask count: BN tokens; 2 TMEM A slots of KA reduction columns per operand; MPC
+// masks per CTA.  n_m = 8 would leave BN = 32 (nine accumulators): instead a cluster of two CTAs
+// splits the masks 4 + 4 (each also forms t), and the pair sums its partial outputs over DSMEM.
 template <int NM> struct TcCfg;
-template <> struct TcCfg<1> { static constexpr int BN = 224, KA = 32; };
-template <> struct TcCfg<2> { static constexpr int BN = 128, KA = 32; };
-template <> struct TcCfg<4> { static constexpr int BN = 64, KA = 32; };
-template <> struct TcCfg<8> { static constexpr int BN = 32, KA = 16; };
+template <> struct TcCfg<1> { static constexpr int BN = 224, KA = 32, MPC = 1; };
+template <> struct TcCfg<2> { static constexpr int BN = 128, KA = 32, MPC = 2; };
+template <> struct TcCfg<4> { static constexpr int BN = 64, KA = 32, MPC = 4; };
+template <> struct TcCfg<8> { static constexpr int BN = 64, KA = 32, MPC = 4; };
 
 constexpr int kTcThreads = 320;
 constexpr int kTcMaskWarps = 8;
@@ -43,8 +45,11 @@ template <int NM> __host__ __device__ constexpr int tc_x_bytes() { return TcCfg<
 template <int NM> __host__ __device__ constexpr int tc_stage_bytes() {
   return tc_x_bytes<NM>() + 128 * kTcK * 2 + 128 * tc_code_words<NM>() * 4;
 }
+template <int NM> __host__ __device__ constexpr int tc_split() { return NM / TcCfg<NM>::MPC; }
+// DSMEM buffer of the mask-split reduction: the partner's fp32 partial outputs [BN][128]
+template <int NM> __host__ __device__ constexpr int tc_red_bytes() { return tc_split<NM>() > 1 ? TcCfg<NM>::BN * 128 * 4 : 0; }
 template <int NM> __host__ __device__ constexpr int tc_tmem_used() {
-  return (NM + 1) * TcCfg<NM>::BN + kTcSA * (NM + 1) * TcCfg<NM>::KA / 2;
+  return (TcCfg<NM>::MPC + 1) * TcCfg<NM>::BN + kTcSA * (TcCfg<NM>::MPC + 1) * TcCfg<NM>::KA / 2;
 }
 static_assert(tc_tmem_used<1>() <= 512 && tc_tmem_used<2>() <= 512 && tc_tmem_used<4>() <= 512 &&
               tc_tmem_used<8>() <= 512, "TMEM budget");
@@ -60,7 +65,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mW,
                const __grid_constant__ CUtensorMap mC) {
   constexpr int BN = TcCfg<NM>::BN, KA = TcCfg<NM>::KA, SA = kTcSA;
-  constexpr int NOP = NM + 1;                              // operands: W and n_m sign-flipped copies
+  constexpr int MPC = TcCfg<NM>::MPC, NSPLIT = tc_split<NM>();
+  constexpr int NOP = MPC + 1;                             // operands: W and this CTA's sign-flipped copies
   constexpr int XB = tc_x_bytes<NM>(), WB = 128 * kTcK * 2, CW = tc_code_words<NM>();
   constexpr int SB = tc_stage_bytes<NM>();
   constexpr int KPS = KA / 16;                             // k16 steps per A-stage
@@ -72,7 +78,8 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = p.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB);
+  float* red = reinterpret_cast<float*>(smem + (size_t)S * SB);           // mask-split partials (rank 0)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB + tc_red_bytes<NM>());
   uint64_t* empty = full + S;
   uint64_t* a_full = empty + S;
   uint64_t* a_empty = a_full + SA;
@@ -82,6 +89,7 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
   const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);   // provably warp-uniform
   const int lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * 128;
+  const int moff = (int)blockIdx.z * MPC;                  // first mask of this CTA (cluster rank z)
   const int d = p.d;
   const int nk16 = d >> 4;                                 // d % 32 == 0
   const int nks = (d + kTcK - 1) / kTcK;                   // shared stages
@@ -102,6 +110,8 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  constexpr int HALF = BN / 2;                             // epilogue tokens per masker group
+  float yp[HALF / 8][8];                                   // this thread's partial outputs
   if (warp == kTcMaskWarps) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
@@ -182,18 +192,18 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
           const uint4 v = *reinterpret_cast<const uint4*>(st + wrow_off + chunk * 16);
           w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
         }
-        uint32_t cw[NM];
+        uint32_t cw[MPC];
         const int grp = (a * KA) >> 5;                     // code group within the stage
         const int wofs = (ks * 2 * NM) % CW;               // stage's first word within the loaded box
 #pragma unroll
-        for (int i = 0; i < NM; ++i)
-          cw[i] = *reinterpret_cast<const uint32_t*>(st + crow_off + (wofs + grp * NM + i) * 4);
+        for (int i = 0; i < MPC; ++i)
+          cw[i] = *reinterpret_cast<const uint32_t*>(st + crow_off + (wofs + grp * NM + moff + i) * 4);
         const int pair0 = (a * KA) & 31 ? 8 : 0;           // first pair of the A-stage in its group
         uint32_t op[NOP][WW];
 #pragma unroll
         for (int q = 0; q < WW; ++q) op[0][q] = w[q];
 #pragma unroll
-        for (int i = 0; i < NM; ++i) {
+        for (int i = 0; i < MPC; ++i) {
 #pragma unroll
           for (int q = 0; q < WW; ++q)                     // pair pair0 + q: bits (pair, pair + 16)
             op[1 + i][q] = sign_flip(w[q], cw[i], 1u << (15 - pair0 - q));
@@ -219,34 +229,62 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
     mbar_wait(acc_full, 0);
     tc_fence_after();
     pdl_wait();                                            // out may be read upstream
-    const int grow = m0 + m;
     const uint32_t lane_base = tmem + lane_off;
-    constexpr int HALF = BN / 2;                           // tokens per masker group
     static_assert(HALF % 8 == 0, "BN / 2 must be a multiple of 8");
-#pragma unroll 1
-    for (int c0 = g * HALF; c0 < (g + 1) * HALF; c0 += 8) {
-      uint32_t tv[8], uv[NM][8];
+#pragma unroll
+    for (int ch = 0; ch < HALF / 8; ++ch) {
+      const int c0 = g * HALF + ch * 8;
+      uint32_t tv[8], uv[MPC][8];
       tmem_ld8(lane_base + c0, tv);
 #pragma unroll
-      for (int i = 0; i < NM; ++i) tmem_ld8(lane_base + (1 + i) * BN + c0, uv[i]);
+      for (int i = 0; i < MPC; ++i) tmem_ld8(lane_base + (1 + i) * BN + c0, uv[i]);
       tmem_ld_wait();
-      float y[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float t = __uint_as_float(tv[q]);
         float acc = 0.f;
 #pragma unroll
-        for (int i = 0; i < NM; ++i) {
+        for (int i = 0; i < MPC; ++i) {
           const float sg = 0.5f * (t + __uint_as_float(uv[i][q]));       // s_i = (t + u_i) / 2
           acc = fmaf(act_g<ACT>(sg), t - sg, acc);                        // g(s_i) (t - s_i)
         }
-        y[q] = acc;
+        yp[ch][q] = acc;
       }
-      if (grow < p.h) {
+      if constexpr (NSPLIT > 1) {
+        if (blockIdx.z == 1) {                             // partial of masks 5..8 -> rank 0's buffer
+#pragma unroll
+          for (int q = 0; q < 8; ++q) st_cluster_f32(red + (c0 + q) * 128 + m, 0, yp[ch][q]);
+        }
+      } else {
+        const int grow = m0 + m;
+        if (grow < p.h) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int tok = n0 + c0 + q;
+            if (tok < p.B) p.out[(size_t)tok * p.h + grow] = __float2bfloat16_rn(yp[ch][q]);
+          }
+        }
+      }
+    }
+  }
+  if constexpr (NSPLIT > 1) {
+    cluster_arrive();                                      // partials delivered (release / acquire)
+    cluster_wait();
+  }
+  if (NSPLIT > 1 && warp < kTcMaskWarps && blockIdx.z == 0) {
+    const int g = warp >> 2;
+    const int m = (warp & 3) * 32 + lane;
+    const int grow = m0 + m;
+    if (grow < p.h) {
+#pragma unroll
+      for (int ch = 0; ch < HALF / 8; ++ch) {
+        const int c0 = g * HALF + ch * 8;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int tok = n0 + c0 + q;
-          if (tok < p.B) p.out[(size_t)tok * p.h + grow] = __float2bfloat16_rn(y[q]);
+          float y = yp[ch][q];
+          if constexpr (NSPLIT > 1) y += red[(c0 + q) * 128 + m];        // masks 1..4 + masks 5..8
+          if (tok < p.B) p.out[(size_t)tok * p.h + grow] = __float2bfloat16_rn(y);
         }
       }
     }

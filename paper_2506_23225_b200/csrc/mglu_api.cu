@@ -330,7 +330,7 @@ cudaError_t run_tc(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const
   p.d = (int)hd->d;
   p.h = (int)hd->h;
   constexpr size_t SB = mglu::tc_stage_bytes<NM>();
-  const size_t fixed = 1024 + 256;                          // alignment slack + barriers / TMEM slot
+  const size_t fixed = 1024 + 256 + mglu::tc_red_bytes<NM>();   // alignment slack + barriers + split buffer
   const size_t cap = (size_t)hd->max_smem_optin;
   if (cap < fixed + 2 * SB) return cudaErrorInvalidConfiguration;
   const int S = (int)std::min<size_t>(6, (cap - fixed) / SB);
@@ -339,8 +339,23 @@ cudaError_t run_tc(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const
   auto kern = mglu::gemm_tc_kernel<NM, ACT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const dim3 grid((unsigned)((B + BN - 1) / BN), (unsigned)((hd->h + 127) / 128));
-  return launch_pdl(kern, grid, dim3(mglu::kTcThreads), smem, st, p, mX, mW, mC);
+  constexpr int NSPLIT = mglu::tc_split<NM>();
+  const dim3 grid((unsigned)((B + BN - 1) / BN), (unsigned)((hd->h + 127) / 128), NSPLIT);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(mglu::kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;          // mask-split pair (n_m = 8) shares DSMEM
+  at[1].val.clusterDim.x = 1;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = NSPLIT;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, p, mX, mW, mC);
 }
 
 template <int NM>
