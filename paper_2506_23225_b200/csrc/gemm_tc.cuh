@@ -37,19 +37,24 @@ template <> struct TcCfg<8> { static constexpr int BN = 64, KA = 32, MPC = 4; };
 constexpr int kTcThreads = 320;
 constexpr int kTcMaskWarps = 8;
 constexpr int kTcK = 64;                        // reduction columns per shared stage
-constexpr int kTcSA = 2;                        // TMEM A slots (one per masker group)
+// TMEM A slots: 4 when the accumulators leave room (small token tiles: deeper masker run-ahead
+// hides the slot round trip), else 2 -- always even, so every slot belongs to one masker group
+template <int NM, int BN> __host__ __device__ constexpr int tc_slots() {
+  return (TcCfg<NM>::MPC + 1) * BN + 4 * (TcCfg<NM>::MPC + 1) * TcCfg<NM>::KA / 2 <= 512 ? 4 : 2;
+}
 
 // mask words per row per stage as loaded by TMA: 2 groups x n_m words, at least 16 bytes
 template <int NM> __host__ __device__ constexpr int tc_code_words() { return 2 * NM < 4 ? 4 : 2 * NM; }
-template <int NM> __host__ __device__ constexpr int tc_x_bytes() { return TcCfg<NM>::BN * kTcK * 2; }
-template <int NM> __host__ __device__ constexpr int tc_stage_bytes() {
-  return tc_x_bytes<NM>() + 128 * kTcK * 2 + 128 * tc_code_words<NM>() * 4;
+// BN = token tile: TcCfg<NM>::BN for prefill, 16 / 32 / 64 for small batches (decode regime)
+template <int BN> __host__ __device__ constexpr int tc_x_bytes() { return BN * kTcK * 2; }
+template <int NM, int BN> __host__ __device__ constexpr int tc_stage_bytes() {
+  return tc_x_bytes<BN>() + 128 * kTcK * 2 + 128 * tc_code_words<NM>() * 4;
 }
 template <int NM> __host__ __device__ constexpr int tc_split() { return NM / TcCfg<NM>::MPC; }
 // DSMEM buffer of the mask-split reduction: the partner's fp32 partial outputs [BN][128]
-template <int NM> __host__ __device__ constexpr int tc_red_bytes() { return tc_split<NM>() > 1 ? TcCfg<NM>::BN * 128 * 4 : 0; }
+template <int NM, int BN> __host__ __device__ constexpr int tc_red_bytes() { return tc_split<NM>() > 1 ? BN * 128 * 4 : 0; }
 template <int NM> __host__ __device__ constexpr int tc_tmem_used() {
-  return (TcCfg<NM>::MPC + 1) * TcCfg<NM>::BN + kTcSA * (TcCfg<NM>::MPC + 1) * TcCfg<NM>::KA / 2;
+  return (TcCfg<NM>::MPC + 1) * TcCfg<NM>::BN + 2 * (TcCfg<NM>::MPC + 1) * TcCfg<NM>::KA / 2;
 }
 static_assert(tc_tmem_used<1>() <= 512 && tc_tmem_used<2>() <= 512 && tc_tmem_used<4>() <= 512 &&
               tc_tmem_used<8>() <= 512, "TMEM budget");
@@ -60,26 +65,26 @@ struct TcParams {
   int stages;
 };
 
-template <int NM, int ACT>
+template <int NM, int ACT, int BN>
 __global__ void __launch_bounds__(kTcThreads, 1)
 gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mW,
                const __grid_constant__ CUtensorMap mC) {
-  constexpr int BN = TcCfg<NM>::BN, KA = TcCfg<NM>::KA, SA = kTcSA;
+  constexpr int KA = TcCfg<NM>::KA, SA = tc_slots<NM, BN>();
+  static_assert((TcCfg<NM>::MPC + 1) * BN + SA * (TcCfg<NM>::MPC + 1) * KA / 2 <= 512, "TMEM budget");
   constexpr int MPC = TcCfg<NM>::MPC, NSPLIT = tc_split<NM>();
   constexpr int NOP = MPC + 1;                             // operands: W and this CTA's sign-flipped copies
-  constexpr int XB = tc_x_bytes<NM>(), WB = 128 * kTcK * 2, CW = tc_code_words<NM>();
-  constexpr int SB = tc_stage_bytes<NM>();
+  constexpr int XB = tc_x_bytes<BN>(), WB = 128 * kTcK * 2, CW = tc_code_words<NM>();
+  constexpr int SB = tc_stage_bytes<NM, BN>();
   constexpr int KPS = KA / 16;                             // k16 steps per A-stage
   constexpr int APS = kTcK / KA;                           // A-stages per shared stage (2 or 4)
   constexpr int WW = KA / 2;                               // bf16 pairs per row and A-stage
   constexpr uint32_t IDESC = idesc_bf16_f32(128, BN);
   constexpr uint32_t A_COL0 = NOP * BN;                    // first TMEM column of the A slots
-  static_assert(APS % SA == 0, "each shared stage holds whole A-slot cycles");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = p.stages;
   float* red = reinterpret_cast<float*>(smem + (size_t)S * SB);           // mask-split partials (rank 0)
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB + tc_red_bytes<NM>());
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB + tc_red_bytes<NM, BN>());
   uint64_t* empty = full + S;
   uint64_t* a_full = empty + S;
   uint64_t* a_empty = a_full + SA;
@@ -145,7 +150,7 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
         const int j = ks * (kTcK / 16) + kk;               // k16 step
         if (j < nk16) {
           const int js = j / KPS;                          // A-stage
-          const int sa = (kk / KPS) % SA;                  // == js % SA
+          const int sa = js % SA;
           if (kk % KPS == 0) {
             mbar_wait(&a_full[sa], (uint32_t)(js / SA) & 1u);
             tc_fence_after();

@@ -314,10 +314,9 @@ bool encode_2d_u32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t row
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int NM, int ACT>
-cudaError_t run_tc(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
-                   cudaStream_t st) {
-  constexpr int BN = mglu::TcCfg<NM>::BN;
+template <int NM, int ACT, int BN>
+cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
+                      cudaStream_t st) {
   CUtensorMap mX, mW, mC;
   const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
   if (!encode_2d_bf16(&mX, x, hd->d, B, mglu::kTcK, BN, sw) ||
@@ -329,14 +328,14 @@ cudaError_t run_tc(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const
   p.B = (int)B;
   p.d = (int)hd->d;
   p.h = (int)hd->h;
-  constexpr size_t SB = mglu::tc_stage_bytes<NM>();
-  const size_t fixed = 1024 + 256 + mglu::tc_red_bytes<NM>();   // alignment slack + barriers + split buffer
+  constexpr size_t SB = mglu::tc_stage_bytes<NM, BN>();
+  const size_t fixed = 1024 + 256 + mglu::tc_red_bytes<NM, BN>();   // alignment slack + barriers + split buffer
   const size_t cap = (size_t)hd->max_smem_optin;
   if (cap < fixed + 2 * SB) return cudaErrorInvalidConfiguration;
-  const int S = (int)std::min<size_t>(6, (cap - fixed) / SB);
+  const int S = (int)std::min<size_t>(8, (cap - fixed) / SB);
   p.stages = S;
   const size_t smem = (size_t)S * SB + fixed;
-  auto kern = mglu::gemm_tc_kernel<NM, ACT>;
+  auto kern = mglu::gemm_tc_kernel<NM, ACT, BN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   constexpr int NSPLIT = mglu::tc_split<NM>();
@@ -356,6 +355,17 @@ cudaError_t run_tc(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const
   cfg.attrs = at;
   cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, p, mX, mW, mC);
+}
+
+// token tile: small batches take the smallest tile that holds them (the MMA work then scales with
+// B and the kernel streams W and the mask words at HBM rate); large batches the TMEM-limited tile
+template <int NM, int ACT>
+cudaError_t run_tc(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
+                   cudaStream_t st) {
+  if (B <= 16) return run_tc_bn<NM, ACT, 16>(hd, x, B, Wt, codes, out, st);
+  if (B <= 32) return run_tc_bn<NM, ACT, 32>(hd, x, B, Wt, codes, out, st);
+  if (B <= 64 || mglu::TcCfg<NM>::BN == 64) return run_tc_bn<NM, ACT, 64>(hd, x, B, Wt, codes, out, st);
+  return run_tc_bn<NM, ACT, mglu::TcCfg<NM>::BN>(hd, x, B, Wt, codes, out, st);
 }
 
 template <int NM>
