@@ -46,7 +46,10 @@
  * caller's next synchronisation, as in CUDA.
  *
  * Threading: a handle is immutable after mglu_create except for mglu_set_path and its internal
- * caches (guarded by a mutex); concurrent mglu_forward calls on different streams are allowed.
+ * caches (guarded by a mutex); concurrent mglu_forward calls on different streams are allowed,
+ * EXCEPT on MGLU_PATH_TCDEC (which AUTO picks for bf16 and 1 <= B <= 64): its CTAs exchange
+ * partial sums through the handle's workspace, so calls on one handle must be stream-ordered --
+ * use one handle per concurrently running stream.
  * Streams are `cudaStream_t` passed as void* (NULL = the legacy default stream).
  */
 #ifndef MGLU_H_
@@ -88,7 +91,8 @@ typedef enum {
   MGLU_PATH_AUTO = 0,
   MGLU_PATH_SIMT = 1,     /* CUDA-core fused masked GEMV (Alg. 1 without split-K), any dtype/B   */
   MGLU_PATH_MMA = 2,      /* register-masked mma.sync GEMV, bf16, streams W+codes once per 8 tok */
-  MGLU_PATH_TCGEN05 = 3   /* tcgen05/TMEM masked GEMM, bf16, prefill / large B                  */
+  MGLU_PATH_TCGEN05 = 3,  /* tcgen05/TMEM masked GEMM, bf16, prefill / large B                  */
+  MGLU_PATH_TCDEC = 4     /* tcgen05 stream-K masked GEMV, bf16, decode 1 <= B <= 64             */
 } mglu_path;
 
 /* Create a handle for one (d, h, n_m, act, dtype) layer on CUDA device `device`.

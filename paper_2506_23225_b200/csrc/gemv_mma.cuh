@@ -36,7 +36,10 @@
 
 namespace mglu {
 
-constexpr int kDecConsumers = 16;                      // consumer warps (4 per SM sub-partition)
+#ifndef MGLU_DEC_CONSUMERS
+#define MGLU_DEC_CONSUMERS 16
+#endif
+constexpr int kDecConsumers = MGLU_DEC_CONSUMERS;      // consumer warps (4 per SM sub-partition)
 constexpr int kDecThreads = (kDecConsumers + 1) * 32;  // + 1 producer warp
 constexpr int kDecFullTiles = kDecConsumers / 2;       // 8-row tiles of a full round (2 warps each)
 constexpr int kDecFullRows = 8 * kDecFullTiles;        // 64
@@ -148,11 +151,12 @@ gemv_mma_kernel(const DecParams p,
   pdl_wait();                                              // x is the predecessor's output
   {
     // x -> smem split by bf16-pair parity: xs[b][parity][pair/2], zero-padded past d
+    // token B is an all-zero row: lanes whose MMA column has no token read it unconditionally
     const int npair = p.xpar * 2 - 16;
-    for (int v = threadIdx.x; v < B * npair; v += kDecConsumers * 32) {
+    for (int v = threadIdx.x; v < (B + 1) * npair; v += kDecConsumers * 32) {
       const int b = v / npair, q = v - b * npair;
       uint32_t val = 0u;
-      if (2 * q < d) val = reinterpret_cast<const uint32_t*>(p.x + (size_t)b * d)[q];
+      if (b < B && 2 * q < d) val = reinterpret_cast<const uint32_t*>(p.x + (size_t)b * d)[q];
       xs[(size_t)(2 * b + (q & 1)) * p.xpar + (q >> 1)] = val;
     }
   }
@@ -178,44 +182,50 @@ gemv_mma_kernel(const DecParams p,
     const int tl = warp / wpt, kp = warp - tl * wpt;        // tile and column part of this warp
     const bool live = tl < ntile;                           // warp-uniform
     const int srow = tl * 8 + prow;                         // row within the round's box
+    // per-round shared-memory offsets (bytes, relative to a stage slot) of this thread's operands
+    // for the four 32-column steps st of a stage: the stage loop then only adds the slot base
+    uint32_t woff[4], coff[4];
+#pragma unroll
+    for (int st = 0; st < 4; ++st) {
+      // A: pairs 4c..4c+3 of step st = one swizzled 16-byte read of W block (2 kp + st/2)
+      woff[st] = swz((uint32_t)(((2 * kp + (st >> 1)) * rows + srow) * 128 + (32 * (st & 1) + 8 * c) * 2), 128);
+      // the step's 32-column group (group st of code block kp): n_m words (16-byte chunks swizzled)
+      coff[st] = (uint32_t)kDecWBytes + swz((uint32_t)((kp * rows + srow) * SPAN + st * 4 * NM), SPAN);
+    }
+    // x: word index of pair 4c of step 0 of stage 0 for this lane's token column (token B = zeros)
+    uint32_t xoff[NB];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      const int tok = min(nb * 4 + (g >> 1), B);
+      xoff[nb] = (uint32_t)((2 * tok + (g & 1)) * p.xpar + kp * 32 + 2 * c) * 4u;
+    }
     for (int ks = 0; ks < nks; ++ks, ++i) {
       mbar_wait(&full[s], ph);
       if (live) {
-        const uint8_t* wst = ring + (size_t)s * SB;
-        const uint8_t* cst = wst + kDecWBytes;
-        const int kbase = ks * 128 * wpt + kp * 128;         // global column of this warp's part
+        // slot base as a provably warp-uniform value: the LDS addresses become [per-thread + uniform]
+        const uint8_t* wst = ring + __shfl_sync(0xffffffffu, s * SB, 0);
+        const uint8_t* xst = reinterpret_cast<const uint8_t*>(xs) + __shfl_sync(0xffffffffu, ks * wpt * 128, 0);
 #pragma unroll
         for (int st = 0; st < 4; ++st) {
-          // A: pairs 4c..4c+3 of the step = one swizzled 16-byte read of W block (2 kp + st/2)
-          const uint32_t wlin = (uint32_t)(((2 * kp + (st >> 1)) * rows + srow) * 128 + (32 * (st & 1) + 8 * c) * 2);
-          const uint4 wq = *reinterpret_cast<const uint4*>(wst + swz(wlin, 128));
-          // mask words of this step's 32-column group (group st of code block kp): n_m words
+          const uint4 wq = *reinterpret_cast<const uint4*>(wst + woff[st]);
           uint32_t mw[NM];
-          {
-            const uint32_t clin = (uint32_t)((kp * rows + srow) * SPAN + st * 4 * NM);
 #pragma unroll
-            for (int q = 0; q < (NM + 3) / 4; ++q) {
-              const uint8_t* cp = cst + swz(clin + 16 * q, SPAN);
-              if constexpr (NM == 1) mw[0] = *reinterpret_cast<const uint32_t*>(cp);
-              else if constexpr (NM == 2) { const uint2 u = *reinterpret_cast<const uint2*>(cp); mw[0] = u.x; mw[1] = u.y; }
-              else {
-                const uint4 u = *reinterpret_cast<const uint4*>(cp);
-                mw[4 * q] = u.x; mw[4 * q + 1] = u.y; mw[4 * q + 2] = u.z; mw[4 * q + 3] = u.w;
-              }
+          for (int q = 0; q < (NM + 3) / 4; ++q) {
+            // n_m = 8: the second 16-byte chunk is the next one in the swizzled span
+            const uint8_t* cp = wst + (q == 0 ? coff[st] : (coff[st] ^ 16u));
+            if constexpr (NM == 1) mw[0] = *reinterpret_cast<const uint32_t*>(cp);
+            else if constexpr (NM == 2) { const uint2 u = *reinterpret_cast<const uint2*>(cp); mw[0] = u.x; mw[1] = u.y; }
+            else {
+              const uint4 u = *reinterpret_cast<const uint4*>(cp);
+              mw[4 * q] = u.x; mw[4 * q + 1] = u.y; mw[4 * q + 2] = u.z; mw[4 * q + 3] = u.w;
             }
           }
           // B: x pairs (4c + parity, 4c + 2 + parity) of the step for this lane's column(s)
           uint32_t xb[NB][2];
 #pragma unroll
           for (int nb = 0; nb < NB; ++nb) {
-            const int tok = nb * 4 + (g >> 1);
-            if (tok < B) {
-              const int gp = (kbase + 32 * st + 8 * c) / 2;    // global pair index of pair 4c
-              const uint2 u = *reinterpret_cast<const uint2*>(xs + (size_t)(2 * tok + (g & 1)) * p.xpar + (gp >> 1));
-              xb[nb][0] = u.x; xb[nb][1] = u.y;
-            } else {
-              xb[nb][0] = 0u; xb[nb][1] = 0u;
-            }
+            const uint2 u = *reinterpret_cast<const uint2*>(xst + xoff[nb] + st * 32);
+            xb[nb][0] = u.x; xb[nb][1] = u.y;
           }
           // t += x W
 #pragma unroll

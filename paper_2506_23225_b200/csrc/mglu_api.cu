@@ -19,6 +19,7 @@
 #include "gemv_mma.cuh"
 #include "gemv_simt.cuh"
 #include "gemm_tc.cuh"
+#include "gemv_tc.cuh"
 #include "pack.cuh"
 
 struct mglu_ctx {
@@ -45,6 +46,11 @@ struct mglu_ctx {
   };
   std::array<DecMaps, 16> dec_cache;
   uint64_t dec_clock = 0;
+  // stream-K decode (tcgen05) workspace: partial accumulators + one flag per CTA (flags are 0
+  // between calls: the owner CTA re-arms them), grown on demand
+  float* sk_ws = nullptr;
+  size_t sk_ws_bytes = 0;
+  uint32_t* sk_flags = nullptr;
 
 };
 
@@ -235,7 +241,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   const int npair = (int)(maxcol / 2);
   p.xpar = npair / 2 + 8;
   constexpr size_t SB = mglu::dec_stage_bytes<NM>();
-  const size_t xbytes = (size_t)2 * B * p.xpar * 4;
+  const size_t xbytes = (size_t)2 * (B + 1) * p.xpar * 4;   // + an all-zero token row
   const size_t partbytes = (size_t)mglu::kDecConsumers * 32 * NB * (NM + 1) * 4;
   const size_t fixed = xbytes + partbytes + 1024;
   const size_t cap = std::min<size_t>((size_t)hd->max_smem_optin, 200 * 1024);
@@ -390,6 +396,99 @@ cudaError_t tc_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const 
   }
 }
 
+// ------------------------------------------------------------------ tcgen05 stream-K decode dispatch
+constexpr int kSkMaxB = 64;
+#ifndef MGLU_SK_MG
+#define MGLU_SK_MG 2
+#endif
+
+bool sk_can_serve(const mglu_ctx* hd, int64_t B) {
+  // 64-column units; mask-word rows of d/32 * n_m u32 words must be 16-byte multiples (TMA)
+  return hd->dtype == MGLU_BF16 && hd->d % 64 == 0 && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 &&
+         B <= kSkMaxB && (hd->n_m < 8 || B <= 32);
+}
+
+// workspace of the stream-K decode path, allocated once at mglu_create for the largest batch the
+// path serves: G x (n_m + 1) x B x 128 fp32 partials and G flags (zeroed; owners re-arm them)
+cudaError_t sk_alloc(mglu_ctx* hd) {
+  const size_t G = (size_t)hd->num_sms;
+  const size_t maxb = hd->n_m == 8 ? 32 : kSkMaxB;
+  cudaError_t e = cudaMalloc(&hd->sk_flags, G * sizeof(uint32_t));
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(hd->sk_flags, 0, G * sizeof(uint32_t));
+  if (e != cudaSuccess) return e;
+  hd->sk_ws_bytes = G * (size_t)(hd->n_m + 1) * maxb * 128 * sizeof(float);
+  e = cudaMalloc(&hd->sk_ws, hd->sk_ws_bytes);
+  if (e != cudaSuccess) hd->sk_ws_bytes = 0;
+  return e;
+}
+
+template <int NM, int BN, int MG, int WQ>
+cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
+                      cudaStream_t st) {
+  using C = mglu::SkCfg<NM, BN, MG, WQ>;
+  CUtensorMap mW, mX, mC;
+  const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
+  constexpr int KB = mglu::kSkKS / 64;
+  if (!encode_3d_blocks(&mW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, 128, KB, sw) ||
+      !encode_3d_blocks(&mX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, hd->d, B, 64, BN, KB, sw) ||
+      !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, C::CW, 128))
+    return cudaErrorInvalidValue;
+  mglu::SkParams p;
+  p.out = (__nv_bfloat16*)out;
+  p.B = (int)B;
+  p.d = (int)hd->d;
+  p.h = (int)hd->h;
+  p.act = hd->act;
+  p.upt = (int)((hd->d + mglu::kSkKS - 1) / mglu::kSkKS);   // a final half unit reads zero-filled boxes
+  const int64_t units = (hd->h + 127) / 128 * p.upt;
+  const int64_t G = std::min<int64_t>(hd->num_sms, units);
+  p.units_base = (int)(units / G);
+  p.units_rem = (int)(units % G);
+  if (!hd->sk_flags || hd->sk_ws_bytes < (size_t)G * C::NOP * B * 128 * sizeof(float)) return cudaErrorInvalidValue;
+  p.ws = hd->sk_ws;
+  p.flags = hd->sk_flags;
+  const size_t fixed = 1024 + 512;                          // alignment slack + barriers + TMEM slot
+  const size_t cap = (size_t)hd->max_smem_optin;
+  if (cap < fixed + 2 * (size_t)C::SB) return cudaErrorInvalidConfiguration;
+  const int S = (int)std::min<size_t>(16, (cap - fixed) / C::SB);
+  p.stages = S;
+  const size_t smem = (size_t)S * C::SB + fixed;
+  auto kern = mglu::gemv_tc_kernel<NM, BN, MG, WQ>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(kern, dim3((unsigned)G), dim3(C::THREADS), smem, st, p, mW, mX, mC);
+}
+
+// masker organisation: MGLU_SK_MG groups x MGLU_SK_WQ warps per lane quarter when the TMEM budget
+// allows (accumulators are per group, >= 2 A slots per group), else fewer groups
+template <int NM, int BN>
+cudaError_t run_sk_mg(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
+                      cudaStream_t st) {
+  if constexpr (mglu::SkCfg<NM, BN, MGLU_SK_MG, MGLU_SK_WQ>::ok)
+    return run_sk_bn<NM, BN, MGLU_SK_MG, MGLU_SK_WQ>(hd, x, B, Wt, codes, out, st);
+  else return run_sk_bn<NM, BN, 1, MGLU_SK_WQ>(hd, x, B, Wt, codes, out, st);
+}
+
+template <int NM>
+cudaError_t run_sk(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
+                   cudaStream_t st) {
+  if (B <= 16) return run_sk_mg<NM, 16>(hd, x, B, Wt, codes, out, st);
+  if (B <= 32) return run_sk_mg<NM, 32>(hd, x, B, Wt, codes, out, st);
+  if constexpr (NM < 8) return run_sk_mg<NM, 64>(hd, x, B, Wt, codes, out, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t sk_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
+                  cudaStream_t st) {
+  switch (hd->n_m) {
+    case 1: return run_sk<1>(hd, x, B, Wt, codes, out, st);
+    case 2: return run_sk<2>(hd, x, B, Wt, codes, out, st);
+    case 4: return run_sk<4>(hd, x, B, Wt, codes, out, st);
+    default: return run_sk<8>(hd, x, B, Wt, codes, out, st);
+  }
+}
+
 mglu_status check_ptrs(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes,
                        const void* out) {
   if (!hd) return MGLU_ERR_INVALID_ARG;
@@ -471,6 +570,17 @@ mglu_status mglu_create(mglu_handle* out, int64_t d, int64_t h, int n_m, int act
   hd->d = d; hd->h = h; hd->n_m = n_m; hd->act = act; hd->dtype = dtype; hd->device = device;
   hd->num_sms = prop.multiProcessorCount;
   hd->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
+  if (dtype == MGLU_BF16) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    const cudaError_t e = sk_alloc(hd);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+      mglu_destroy(hd);
+      return e == cudaErrorMemoryAllocation ? MGLU_ERR_OOM : MGLU_ERR_CUDA;
+    }
+  }
   *out = hd;
   return MGLU_OK;
 }
@@ -482,13 +592,15 @@ mglu_status mglu_destroy(mglu_handle hd) {
   cudaSetDevice(hd->device);
   if (hd->x_stage) cudaFree(hd->x_stage);
   if (hd->y_stage) cudaFree(hd->y_stage);
+  if (hd->sk_ws) cudaFree(hd->sk_ws);
+  if (hd->sk_flags) cudaFree(hd->sk_flags);
   cudaSetDevice(prev);
   delete hd;
   return MGLU_OK;
 }
 
 mglu_status mglu_set_path(mglu_handle hd, int path) {
-  if (!hd || path < MGLU_PATH_AUTO || path > MGLU_PATH_TCGEN05) return MGLU_ERR_INVALID_ARG;
+  if (!hd || path < MGLU_PATH_AUTO || path > MGLU_PATH_TCDEC) return MGLU_ERR_INVALID_ARG;
   std::lock_guard<std::mutex> g(hd->mu);
   hd->path = path;
   return MGLU_OK;
@@ -535,6 +647,14 @@ mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* W
       return set_err(hd, MGLU_ERR_UNSUPPORTED, "tcgen05 path needs bf16 and d * n_m % 128 == 0");
     }
     e = tc_nm(hd, x, B, Wt, packed, out, st);
+    launches = 1;
+  } else if (path == MGLU_PATH_TCDEC) {
+    if (!sk_can_serve(hd, B)) {
+      if (prev != hd->device) cudaSetDevice(prev);
+      return set_err(hd, MGLU_ERR_UNSUPPORTED,
+                     "tcgen05 decode path needs bf16, 1 <= B <= 64 (32 for n_m = 8), d % 64 == 0, d * n_m % 128 == 0");
+    }
+    e = sk_nm(hd, x, B, Wt, packed, out, st);
     launches = 1;
   } else {
     e = hd->dtype == MGLU_BF16

@@ -140,12 +140,9 @@ int run(long long* d_out) {
 int main() {
   long long* d_out;
   CK(cudaMalloc(&d_out, 148 * sizeof(long long)));
-  // store interference without handshake: ST st8 per warp per k16 step
-  run<4, 64, 5, 1, 0, 1>(d_out); run<4, 64, 5, 1, 0, 2>(d_out); run<4, 64, 5, 1, 0, 5>(d_out); run<4, 64, 5, 1, 0, 10>(d_out);
-  // handshake only, and handshake + stores (per commit)
-  run<5, 64, 5, 1, 1, 0>(d_out); run<5, 64, 5, 2, 1, 0>(d_out); run<5, 64, 5, 2, 1, 5>(d_out); run<5, 64, 5, 2, 1, 10>(d_out);
-  run<5, 64, 5, 4, 1, 0>(d_out); run<5, 64, 5, 4, 1, 20>(d_out);
-  run<5, 32, 9, 1, 1, 0>(d_out); run<5, 32, 9, 2, 1, 0>(d_out); run<5, 32, 9, 2, 1, 18>(d_out);
-  run<5, 96, 4, 2, 1, 8>(d_out); run<5, 80, 5, 2, 1, 10>(d_out);
+  run<0, 16, 5, 1, 0>(d_out);
+  // TS MMAs (N = 16, 5 per k16 step) with 4 warps concurrently tcgen05.st-ing ST x8 columns per step
+  run<4, 16, 5, 1, 0, 1>(d_out); run<4, 16, 5, 1, 0, 2>(d_out); run<4, 16, 5, 1, 0, 5>(d_out); run<4, 16, 5, 1, 0, 10>(d_out);
+  run<4, 64, 5, 1, 0, 5>(d_out);
   return 0;
 }
