@@ -310,9 +310,10 @@ def run_mglu(args, ws, rank, local):
         build()
     barrier(ws)
     from paper_2506_23225_b200.mglu import Mglu
+    from paper_2506_23225_b200.shard import shard_bounds
     d, h, n_m, B, act, desc = WORKLOADS[args.workload]
-    # column shard of h (no exchange on the hot path)
-    lo, hi = rank * h // ws, (rank + 1) * h // ws
+    # column shard of h (no exchange on the hot path): this rank's rows of Wt and of the codes
+    lo, hi = shard_bounds(h, ws, rank)
     h_loc = hi - lo
     L = args.layers
     x, layers = make_layers(d, h_loc, n_m, B, L, seed=0, rank=rank)

@@ -1,0 +1,61 @@
+"""Column (h) sharding of one MGLU up-projection layer across the ranks of a process group.
+
+Eq. 3 is evaluated independently for every output column j: t_j, s_i,j and v_i,j
+read only row j of Wt and row j of the packed codes.  A layer therefore shards along h with no
+exchange on the hot path (north_star): rank g of G owns the contiguous rows
+[lo_g, hi_g) of Wt and of the packed codes -- in the pair-split bit-plane layout (R3)
+row j owns bytes [j*d*n_m/8, (j+1)*d*n_m/8), so a shard is a pointer offset into both tensors --
+and runs an ordinary ``Mglu(d, hi_g - lo_g, n_m)`` handle on its rows.  x is replicated.
+
+The one collective is ``gather_columns``: an all-gather of the h-sliced outputs into [B][h], used
+only to check the full output (an FFN's row-parallel down-projection would consume the slices
+directly).  Unequal shards (h % G != 0) are padded to the largest slice for the
+all-gather and trimmed afterwards.
+
+This module is host logic only (index arithmetic, views and torch.distributed calls); every
+arithmetic step of the forward pass runs in libmglu's kernels.
+"""
+from __future__ import annotations
+
+import torch
+
+
+def shard_bounds(h: int, world: int, rank: int) -> tuple[int, int]:
+    """Rows [lo, hi) of rank `rank`: contiguous, sizes differ by at most one row, rank order."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    return rank * h // world, (rank + 1) * h // world
+
+
+def code_bytes_per_row(d: int, n_m: int) -> int:
+    """Bytes of packed codes per Wt row: d * n_m / 8 (d % 32 == 0, reading R3)."""
+    if d % 32:
+        raise ValueError("d must be a multiple of 32")
+    return d * n_m // 8
+
+
+def shard_layer(Wt: torch.Tensor, packed: torch.Tensor, n_m: int, world: int, rank: int):
+    """Views of this rank's rows of Wt [h][d] and of the packed codes (no copy)."""
+    h, d = Wt.shape
+    lo, hi = shard_bounds(h, world, rank)
+    rb = code_bytes_per_row(d, n_m)
+    if packed.numel() != h * rb:
+        raise ValueError("packed codes size mismatch")
+    return Wt[lo:hi], packed[lo * rb:hi * rb]
+
+
+def gather_columns(y_local: torch.Tensor, h: int, group=None) -> torch.Tensor:
+    """All-gather the column slices y_g [B][hi_g - lo_g] of every rank into y [B][h]."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    B = y_local.shape[0]
+    width = max(shard_bounds(h, world, r)[1] - shard_bounds(h, world, r)[0] for r in range(world))
+    buf = torch.zeros((B, width), dtype=y_local.dtype, device=y_local.device)
+    buf[:, :y_local.shape[1]] = y_local
+    parts = [torch.empty((B, width), dtype=y_local.dtype, device=y_local.device) for _ in range(world)]
+    dist.all_gather(parts, buf.contiguous(), group=group)        # NCCL over NVLink, or gloo on CPU
+    cols = []
+    for r in range(world):
+        lo, hi = shard_bounds(h, world, r)
+        cols.append(parts[r][:, :hi - lo])
+    return torch.cat(cols, dim=1)

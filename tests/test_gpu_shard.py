@@ -1,0 +1,65 @@
+"""Column-shard parity on one GPU: G handles Mglu(d, h/G) each run on their row
+slice (pointer offsets into Wt and the packed codes, paper_2506_23225_b200.shard) and the
+concatenated outputs equal the unsharded layer -- bit-identically on the tcgen05 tile path (a
+row's reduction order does not depend on its neighbours) and within the bf16 bound, against the
+oracle, on the decode path (whose row-to-warp schedule depends on the CTA's row count)."""
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import TIGHT, make_inputs, normwise_err, oracle, oracle_inputs, to_device
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_23225_b200.build import build
+    build()
+
+
+def _sharded(x, Wt, packed, n_m, G, path="auto"):
+    from paper_2506_23225_b200.mglu import Mglu
+    from paper_2506_23225_b200.shard import shard_bounds, shard_layer
+    h, d = Wt.shape
+    outs = []
+    for r in range(G):
+        W_r, p_r = shard_layer(Wt, packed, n_m, G, r)
+        lo, hi = shard_bounds(h, G, r)
+        layer = Mglu(d, hi - lo, n_m, act="swish", dtype="bf16", path=path)
+        outs.append(layer.forward(x, W_r, p_r))
+        layer.close()
+    return torch.cat(outs, dim=1)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_tile_path_shards_bit_identical(G):
+    from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
+    d, h, n_m, B = 1024, 1024, 4, 200
+    inp = make_inputs(40 + G, B=B, d=d, h=h, n_m=n_m, dtype="bf16")
+    x, Wt = to_device(inp, "bf16")
+    packed = torch.from_numpy(mglu_pack_masks_host(inp["bits"])).cuda()
+    full = Mglu(d, h, n_m, act="swish", dtype="bf16", path="tcgen05").forward(x, Wt, packed)
+    assert torch.equal(_sharded(x, Wt, packed, n_m, G, path="tcgen05"), full)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_decode_shards_match_oracle(G):
+    from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
+    d, h, n_m, B = 4096, 14336, 4, 1
+    inp = make_inputs(0, B=B, d=d, h=h, n_m=n_m, dtype="bf16")
+    x, Wt = to_device(inp, "bf16")
+    packed = torch.from_numpy(mglu_pack_masks_host(inp["bits"])).cuda()
+    y = _sharded(x, Wt, packed, n_m, G).float().cpu().numpy().astype(np.float64)
+    full = Mglu(d, h, n_m, act="swish", dtype="bf16").forward(x, Wt, packed).float().cpu().numpy()
+    rng = np.random.default_rng(G)
+    # every shard boundary and a random sample
+    bounds = [r * h // G for r in range(G)]
+    cols = np.unique(np.concatenate([bounds, np.array(bounds[1:]) - 1, [h - 1], rng.choice(h, 256, replace=False)]))
+    xo, Wo = oracle_inputs(inp, "bf16")
+    o = oracle()
+    ref = o.forward(xo, Wo[cols], cols, o.pack(inp["bits"]), n_m, 1)
+    assert normwise_err(y[:, cols], ref) <= TIGHT["bf16"]
+    assert normwise_err(y, full) <= TIGHT["bf16"]
