@@ -47,7 +47,7 @@
  *
  * Threading: a handle is immutable after mglu_create except for mglu_set_path and its internal
  * caches (guarded by a mutex); concurrent mglu_forward calls on different streams are allowed,
- * EXCEPT on MGLU_PATH_TCDEC (which AUTO picks for bf16 and 1 <= B <= 64): its CTAs exchange
+ * EXCEPT on MGLU_PATH_TCDEC (which AUTO picks for bf16 and 5 <= B <= 24): its CTAs exchange
  * partial sums through the handle's workspace, so calls on one handle must be stream-ordered --
  * use one handle per concurrently running stream.
  * Streams are `cudaStream_t` passed as void* (NULL = the legacy default stream).
@@ -84,7 +84,8 @@ typedef enum {
 
 typedef enum { MGLU_BF16 = 0, MGLU_F32 = 1 } mglu_dtype;
 
-/* Kernel regime.  AUTO picks by dtype and B.  The others force one
+/* Kernel regime.  AUTO picks by dtype and B (bf16 B <= 4 MMA, 5..24 TCDEC,
+ * larger TCGEN05; fp32 SIMT; a path that refuses the shape falls through).  The others force one
  * kernel (for tests and benchmarks); forcing a path that cannot serve the configuration makes
  * mglu_forward return MGLU_ERR_UNSUPPORTED. */
 typedef enum {

@@ -41,7 +41,7 @@
 namespace mglu {
 
 #ifndef MGLU_SK_KS
-#define MGLU_SK_KS 128
+#define MGLU_SK_KS 256
 #endif
 #ifndef MGLU_SK_KA
 #define MGLU_SK_KA 32
@@ -427,6 +427,298 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
         if (g_sktrace[e][i]) printf("SKT %d %d %u\n", e, i, g_sktrace[e][i]);
   }
 #endif
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Variant 1: a dedicated MMA warp and ONE shared accumulator set (double-buffered when it fits):
+// masker groups arrive on a per-slot a_full, the MMA warp waits it and issues all (n_m + 1) TS MMAs
+// of the A-stage (W itself is operand 0 in the slot, so no MMA reads A from shared memory).
+template <int NM, int BN, int MG> struct Sk1Cfg {
+  static constexpr int NOP = NM + 1;
+  static constexpr int KA = NM == 8 ? 16 : MGLU_SK_KA;
+  static constexpr int SLOT = NOP * KA / 2;
+  static constexpr int ACC = NOP * BN;
+  static constexpr int NACC = 2 * ACC + 2 * MG * SLOT <= 512 ? 2 : 1;
+  static constexpr int SA_FIT = (512 - NACC * ACC) / SLOT / MG * MG;
+  static constexpr int SA = SA_FIT > 4 * MG ? 4 * MG : SA_FIT;
+  static constexpr int WPS = kSkKS / 32 * NM;
+  static constexpr int CW = WPS < 4 ? 4 : WPS;
+  static constexpr int WB = kSkKS / 64 * 128 * 128;
+  static constexpr int XB = kSkKS / 64 * BN * 128;
+  static constexpr int CB = 128 * CW * 4;
+  static constexpr int SB = (WB + XB + CB + 1023) / 1024 * 1024;
+  static constexpr int THREADS = (4 * MG + 6) * 32;
+  static constexpr bool ok = SA >= MG && kSkKS / KA >= MG && (kSkKS / KA) % MG == 0;
+};
+
+template <int NM, int BN, int MG>
+__global__ void __launch_bounds__(Sk1Cfg<NM, BN, MG>::THREADS, 1)
+gemv_tc1_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const __grid_constant__ CUtensorMap mX,
+                const __grid_constant__ CUtensorMap mC) {
+  using C = Sk1Cfg<NM, BN, MG>;
+  constexpr int NOP = C::NOP, KA = C::KA, SLOT = C::SLOT, SA = C::SA, NACC = C::NACC, ACC = C::ACC;
+  constexpr int WPS = C::WPS, CW = C::CW, WB = C::WB, XB = C::XB, SB = C::SB;
+  constexpr int APS = kSkKS / KA, WW = KA / 2;
+  constexpr uint32_t IDESC = idesc_bf16_f32(128, BN);
+  constexpr uint32_t A_COL0 = NACC * ACC;
+  constexpr int kTma = 4 * MG, kMma = 4 * MG + 1, kEpi0 = 4 * MG + 2;
+  static_assert(C::ok, "TMEM budget");
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int S = p.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB);
+  uint64_t* empty = full + S;
+  uint64_t* a_full = empty + S;
+  uint64_t* a_empty = a_full + SA;
+  uint64_t* acc_full = a_empty + SA;
+  uint64_t* acc_empty = acc_full + NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NACC);
+
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
+  const int lane = threadIdx.x & 31;
+  const int cta = blockIdx.x;
+  const int u0 = sk_unit0(p, cta);
+  const int u1 = u0 + p.units_base + (cta < p.units_rem ? 1 : 0);
+  const int upt = p.upt;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < SA; ++s) { mbar_init(&a_full[s], 4); mbar_init(&a_empty[s], 1); }
+    for (int s = 0; s < NACC; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 4); }
+    mbar_fence_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();
+
+  if (warp == kTma) {
+    if (lane == 0) {
+      prefetch_tmap(&mW);
+      prefetch_tmap(&mC);
+      prefetch_tmap(&mX);
+      const uint64_t pol = policy_evict_first();
+      const int n = u1 - u0;
+      const int pre = n < S ? n : S;
+      for (int i = 0; i < pre; ++i) {
+        const int u = u0 + i, tile = u / upt, ks = u - tile * upt;
+        uint8_t* st = smem + (size_t)i * SB;
+        mbar_arrive_expect_tx(&full[i], (uint32_t)(WB + XB + C::CB));
+        tma_load_3d_hint(st, &mW, 0, tile * 128, ks * (kSkKS / 64), &full[i], pol);
+        tma_load_2d_hint(st + WB + XB, &mC, (ks * WPS) / CW * CW, tile * 128, &full[i], pol);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) {
+        const int ks = (u0 + i) % upt;
+        tma_load_3d(smem + (size_t)i * SB + WB, &mX, 0, 0, ks * (kSkKS / 64), &full[i]);
+      }
+      int s = pre % S;
+      uint32_t ph = pre == S ? 1u : 0u;
+      for (int i = pre; i < n; ++i) {
+        const int u = u0 + i, tile = u / upt, ks = u - tile * upt;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + (size_t)s * SB;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(WB + XB + C::CB));
+        tma_load_3d_hint(st, &mW, 0, tile * 128, ks * (kSkKS / 64), &full[s], pol);
+        tma_load_3d(st + WB, &mX, 0, 0, ks * (kSkKS / 64), &full[s]);
+        tma_load_2d_hint(st + WB + XB, &mC, (ks * WPS) / CW * CW, tile * 128, &full[s], pol);
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == kMma) {
+    int s = 0, js = 0, set = 0;
+    uint32_t ph = 0;
+    uint32_t use_a = 0u, use_b = 0u;                   // completed uses of accumulator set 0 / 1
+    for (int u = u0; u < u1; ++u) {
+      const bool seg_first = u == u0 || u % upt == 0;
+      const bool seg_last = u == u1 - 1 || u % upt == upt - 1;
+      if (seg_first) {
+        mbar_wait(&acc_empty[set], ((set ? use_b : use_a) & 1u) ^ 1u);
+        tc_fence_after();
+      }
+      const uint32_t st = smem_u32(smem + (size_t)s * SB);
+      const uint32_t dacc = tmem + (uint32_t)(set * ACC);
+#pragma unroll
+      for (int a = 0; a < APS; ++a, ++js) {
+        const int sa = js % SA;
+        mbar_wait(&a_full[sa], (uint32_t)(js / SA) & 1u);   // implies full[s]: the maskers waited it
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < KA / 16; ++kk) {
+            const int k16 = a * (KA / 16) + kk;
+            const uint64_t bdesc = smem_desc_kmajor(st + WB + (k16 >> 2) * BN * 128, 128) + (uint64_t)((k16 & 3) * 2);
+            const uint32_t accum = (seg_first && k16 == 0) ? 0u : 1u;
+            const uint32_t asl = tmem + A_COL0 + (uint32_t)(sa * SLOT + kk * 8);
+#pragma unroll
+            for (int o = 0; o < NOP; ++o)
+              tc_mma_ts(dacc + (uint32_t)(o * BN), asl + (uint32_t)(o * WW), bdesc, IDESC, accum);
+          }
+          tc_commit(&a_empty[sa]);
+          if (a == APS - 1) tc_commit(&empty[s]);
+          if (a == APS - 1 && seg_last) tc_commit(&acc_full[set]);
+        }
+        __syncwarp();
+      }
+      if (seg_last) { if (set) ++use_b; else ++use_a; if (NACC == 2) set ^= 1; }
+      if (++s == S) { s = 0; ph ^= 1; }
+    }
+  } else if (warp < 4 * MG) {
+    const int g = warp >> 2;
+    const int m = (warp & 3) * 32 + lane;
+    const uint32_t a_lane = tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL0;
+    int s = 0, js = 0;
+    uint32_t ph = 0;
+    for (int u = u0; u < u1; ++u) {
+      const int ks = u % upt;
+      mbar_wait(&full[s], ph);
+      const uint8_t* st = smem + (size_t)s * SB;
+      const int wofs = (ks * WPS) % CW;
+#pragma unroll
+      for (int a = 0; a < APS; ++a, ++js) {
+        if (a % MG != g) continue;
+        const int col = a * KA;
+        uint32_t w[WW];
+#pragma unroll
+        for (int c = 0; c < KA / 8; ++c) {
+          const uint32_t chunk = (uint32_t)(((col & 63) >> 3) + c) ^ (uint32_t)(m & 7);
+          const uint4 v = *reinterpret_cast<const uint4*>(st + (col >> 6) * 16384 + m * 128 + chunk * 16);
+          w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
+        }
+        uint32_t cw[NM];
+        const uint8_t* crow = st + WB + XB + m * CW * 4 + (wofs + (col >> 5) * NM) * 4;
+        if constexpr (NM == 1) cw[0] = *reinterpret_cast<const uint32_t*>(crow);
+        else if constexpr (NM == 2) { const uint2 v = *reinterpret_cast<const uint2*>(crow); cw[0] = v.x; cw[1] = v.y; }
+        else {
+#pragma unroll
+          for (int q = 0; q < NM / 4; ++q) {
+            const uint4 v = *reinterpret_cast<const uint4*>(crow + 16 * q);
+            cw[4 * q] = v.x; cw[4 * q + 1] = v.y; cw[4 * q + 2] = v.z; cw[4 * q + 3] = v.w;
+          }
+        }
+        const int pair0 = (col & 31) >> 1;
+        const int sa = js % SA;
+        mbar_wait(&a_empty[sa], ((uint32_t)(js / SA) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t a0 = a_lane + (uint32_t)(sa * SLOT);
+        tmem_st_n<WW>(a0, w);
+#pragma unroll
+        for (int i = 0; i < NM; ++i) {
+          uint32_t op[WW];
+#pragma unroll
+          for (int q = 0; q < WW; ++q) op[q] = sign_flip(w[q], cw[i], 1u << (15 - pair0 - q));
+          tmem_st_n<WW>(a0 + (uint32_t)((1 + i) * WW), op);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[sa]);
+      }
+      if (++s == S) { s = 0; ph ^= 1; }
+    }
+  } else if (warp >= kEpi0) {
+    const int quarter = warp & 3;
+    const int m = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const int B = p.B;
+    constexpr int CH = 4;
+    const int nch = (B + CH - 1) / CH;
+    pdl_wait();
+    int set = 0;
+    uint32_t use_a = 0u, use_b = 0u;                   // completed uses of accumulator set 0 / 1
+    int u = u0;
+    while (u < u1) {
+      const int tile = u / upt;
+      const int tile_end = (tile + 1) * upt;
+      const int seg_end = u1 < tile_end ? u1 : tile_end;
+      const bool owner = u == tile * upt;
+      const bool whole = owner && seg_end == tile_end;
+      mbar_wait(&acc_full[set], (set ? use_b : use_a) & 1u);
+      tc_fence_after();
+      const uint32_t abase = lane_base + (uint32_t)(set * ACC);
+      const int grow = tile * 128 + m;
+      int ncon = 0;
+      if (owner && !whole) {
+        while (cta + 1 + ncon < (int)gridDim.x && sk_unit0(p, cta + 1 + ncon) < tile_end) ++ncon;
+        for (int k = 1; k <= ncon; ++k) {
+          uint32_t polls = 0;
+          while (ld_acquire_u32(p.flags + cta + k) == 0u) {
+            if (++polls == (1u << 26)) __trap();
+            __nanosleep(64);
+          }
+        }
+      }
+      for (int ch = 0; ch < nch; ++ch) {
+        float f[NOP][CH];
+#pragma unroll
+        for (int o = 0; o < NOP; ++o) {
+          uint32_t v[CH];
+          tmem_ld4(abase + (uint32_t)(o * BN + ch * CH), v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < CH; ++q) f[o][q] = __uint_as_float(v[q]);
+        }
+        if (!owner) {
+          float* wsp = p.ws + (size_t)cta * NOP * B * 128 + m;
+#pragma unroll
+          for (int o = 0; o < NOP; ++o)
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+              const int tok = ch * CH + q;
+              if (tok < B) __stcg(wsp + ((size_t)o * B + tok) * 128, f[o][q]);
+            }
+          continue;
+        }
+        for (int k = 1; k <= ncon; ++k) {
+          const float* wsp = p.ws + (size_t)(cta + k) * NOP * B * 128 + m;
+#pragma unroll
+          for (int o = 0; o < NOP; ++o)
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+              const int tok = ch * CH + q;
+              if (tok < B) f[o][q] += __ldcg(wsp + ((size_t)o * B + tok) * 128);
+            }
+        }
+        if (grow < p.h) {
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            const int tok = ch * CH + q;
+            if (tok < B) {
+              const float t = f[0][q];
+              float y = 0.f;
+#pragma unroll
+              for (int i = 0; i < NM; ++i) {
+                const float sg = 0.5f * (t + f[1 + i][q]);
+                y = fmaf(act_rt(p.act, sg), t - sg, y);
+              }
+              p.out[(size_t)tok * p.h + grow] = __float2bfloat16_rn(y);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[set]);
+      if (!owner) {
+        __threadfence();
+        named_bar_sync(15, 128);
+        if (warp == kEpi0 && lane == 0) st_release_u32(p.flags + cta, 1u);
+      } else if (ncon) {
+        named_bar_sync(15, 128);
+        if (warp == kEpi0)
+          for (int k = lane; k < ncon; k += 32) p.flags[cta + 1 + k] = 0u;
+      }
+      if (set) ++use_b; else ++use_a;
+      if (NACC == 2) set ^= 1;
+      u = seg_end;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 

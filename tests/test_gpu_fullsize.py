@@ -1,5 +1,5 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (AUTO
-dispatch -> the MMA decode kernel), checked on sampled output columns the oracle computes one
+dispatch -> the MMA decode kernel at B = 1, the stream-K tcgen05 GEMV at B = 8), checked on sampled output columns the oracle computes one
 by one, plus a one-hot decode probe on sampled k."""
 import numpy as np
 import pytest
@@ -33,7 +33,7 @@ def test_full_size_sampled_columns(name, d, h, n_m, B):
     packed = torch.from_numpy(packed_np).cuda()
     layer = Mglu(d, h, n_m, act="swish", dtype="bf16")
     y = layer.forward(x, Wt, packed).float().cpu().numpy().astype(np.float64)
-    assert layer.last_path() == "mma"
+    assert layer.last_path() == ("mma" if B <= 4 else "tcdec")     # AUTO crossovers
     rng = np.random.default_rng(1)
     cols = np.unique(np.concatenate([[0, 1, h // 2, h - 2, h - 1], rng.choice(h, 384, replace=False)]))
     xo, Wo = oracle_inputs(inp, "bf16")

@@ -91,7 +91,7 @@ def test_tc_deterministic_and_auto():
     packed = torch.from_numpy(mglu_pack_masks_host(inp["bits"])).cuda()
     layer = Mglu(1024, 300, 4, dtype="bf16")
     y0 = layer.forward(x, Wt, packed).clone()
-    assert layer.last_path() == "tcgen05"                          # AUTO: B > 8 -> tensor cores
+    assert layer.last_path() == "tcgen05"                          # AUTO: B > 24 -> tile GEMM
     for _ in range(3):
         assert torch.equal(layer.forward(x, Wt, packed), y0)
 
