@@ -1,5 +1,5 @@
-// gemv_tc.cuh -- decode / small-batch regime (1 <= B <= 64) on the 5th-generation tensor cores:
-// a persistent, stream-K balanced, TMA-fed masked GEMV.  MGLU_PATH_TCDEC.
+// gemv_tc.cuh -- decode / small-batch regime on the 5th-generation tensor cores: a persistent,
+// stream-K balanced, TMA-fed masked GEMV.  MGLU_PATH_TCDEC (AUTO for 5 <= B <= 24).
 //
 // What it computes is Eq. 3 per token row, by Alg. 1's single pass: W and
 // the packed codes stream HBM -> SM exactly once per call, the unmasked product
@@ -20,18 +20,21 @@
 //
 // Roles (warp-specialised, one CTA per SM):
 //   * warps [0, 4 MG): MG masker groups of 4 warps (one per TMEM lane quarter, thread = tile row).
-//     Group g owns the TMEM A-stages js = g (mod MG): it reads its row's KA columns of W and the
-//     row's mask words from shared memory, writes W and its n_m sign-flipped copies (one IMAD + one
-//     LOP3 per bf16 pair and mask, see sign_flip) into one of its A slots with tcgen05.st (TS form:
-//     the operands never go back to shared memory), and after a named barrier over the group its leader
-//     issues the (n_m + 1) x KA/16 MMAs of the A-stage itself (M = 128, N = BN, K = 16, A = the slot,
-//     B = x) into the GROUP's own fp32 accumulators.  Issuing from the producer of the operands
-//     removes the masker -> MMA-warp mbarrier round trip, which probes showed dominates at N = 16.
+//     Group g owns the KA-column A-stages a = g (mod MG) of every unit: it reads its row's W and
+//     mask words from shared memory and writes W itself plus the n_m sign-flipped copies (one IMAD +
+//     one LOP3 per bf16 pair and mask, see sign_flip) into a TMEM A slot with tcgen05.st, then
+//     arrives on the slot's a_full.  Every MMA therefore reads A from TMEM (the TS form: probes
+//     showed an M=128, N=16 MMA with A in shared memory costs ~4x one with A in TMEM).
 //   * warp 4 MG: TMA producer -- W (3-D box: KS/64 blocks x 128 rows x 64 columns, 128B swizzle),
 //     the tile rows' mask words and x (KS/64 blocks x BN tokens x 64 columns) into an mbarrier ring.
 //     W and the codes stream before griddepcontrol.wait (PDL: constant weights), x after it.
-//   * warps 4 MG + 1 .. 4 MG + 4: epilogue -- tcgen05.ld of the MG group accumulators (summed in
-//     group order), partial publishing or owner fix-up, Eq. 3, bf16 stores.
+//   * warp 4 MG + 1: MMA issuer -- per A-stage (n_m + 1) x KA/16 MMAs (M = 128, N = BN, K = 16,
+//     bf16 -> fp32) into an accumulator set of (n_m + 1) x BN TMEM columns (double-buffered when it
+//     fits), committing the slot back to the maskers and the stage back to the producer.
+//   * warps 4 MG + 2 .. 4 MG + 5: epilogue -- tcgen05.ld of the accumulators, partial publishing or
+//     owner fix-up, Eq. 3, bf16 stores.
+// Variants measured on the way (a per-group MMA issue, wider masker groups, SS operands, 64- and
+// 128-column units) are logged in profiles/r01_tcdec_experiments.txt.
 #pragma once
 #include "common.cuh"
 #include "mma_mask.cuh"
@@ -46,37 +49,7 @@ namespace mglu {
 #ifndef MGLU_SK_KA
 #define MGLU_SK_KA 32
 #endif
-#ifndef MGLU_SK_ABL
-#define MGLU_SK_ABL 0   // timing ablations only (wrong results): 1 no MMA, 2 no MMA + no tcgen05.st, 3 no masking math
-#endif
-#ifndef MGLU_SK_NOX
-#define MGLU_SK_NOX 0   // timing ablation: no x loads
-#endif
-#ifndef MGLU_SK_WQ
-#define MGLU_SK_WQ 1
-#endif
 constexpr int kSkKS = MGLU_SK_KS;   // reduction columns per unit (= shared-memory stage)
-
-// geometry of one instantiation: NM masks, BN token columns, MG masker groups
-template <int NM, int BN, int MG, int WQ_ = MGLU_SK_WQ> struct SkCfg {
-  static constexpr int NOP = NM + 1;                       // operands / accumulators: t, u_1..u_nm
-  static constexpr int KA = NM == 8 ? 16 : MGLU_SK_KA;     // reduction columns per TMEM A-stage
-  static constexpr int SLOT = NOP * KA / 2;                // TMEM columns of one A slot (W + masked copies)
-  static constexpr int ACC = NOP * BN;                     // TMEM columns of one group's accumulators
-  static constexpr int SAG_FIT = (512 - MG * ACC) / (MG * SLOT);
-  static constexpr int SAG = SAG_FIT > 2 ? 2 : SAG_FIT;   // A slots per masker group
-  static constexpr int WPS = kSkKS / 32 * NM;              // mask words per row and stage
-  static constexpr int CW = WPS < 4 ? 4 : WPS;             // words per row in the TMA box (>= 16 B)
-  static constexpr int WB = kSkKS / 64 * 128 * 128;        // W bytes per stage
-  static constexpr int XB = kSkKS / 64 * BN * 128;         // x bytes per stage
-  static constexpr int CB = 128 * CW * 4;                  // mask-word bytes per stage
-  static constexpr int SB = (WB + XB + CB + 1023) / 1024 * 1024;
-  static constexpr int WQ = WQ_;                           // masker warps per TMEM lane quarter and group
-  static constexpr int PPW = KA / 2 / WQ;                  // bf16 pairs per masker warp and A-stage
-  static constexpr int GW = 4 * WQ;                        // warps per masker group
-  static constexpr int THREADS = (GW * MG + 5) * 32;
-  static constexpr bool ok = SAG >= 1 && kSkKS / KA >= MG && (kSkKS / KA) % MG == 0 && (PPW == 4 || PPW % 8 == 0);
-};
 
 struct SkParams {
   __nv_bfloat16* out;   // [B][h]
@@ -111,330 +84,8 @@ __device__ __forceinline__ float act_rt(int act, float z) {
   }
 }
 
-#ifdef MGLU_SK_TRACE
-__device__ uint32_t g_sktrace[8][256];
-__device__ unsigned int g_skcall;
-#endif
-
-template <int NM, int BN, int MG, int WQ>
-__global__ void __launch_bounds__(SkCfg<NM, BN, MG, WQ>::THREADS, 1)
-gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const __grid_constant__ CUtensorMap mX,
-               const __grid_constant__ CUtensorMap mC) {
-  using C = SkCfg<NM, BN, MG, WQ>;
-  constexpr int NOP = C::NOP, KA = C::KA, SLOT = C::SLOT, SAG = C::SAG, ACC = C::ACC;
-  constexpr int WPS = C::WPS, CW = C::CW, WB = C::WB, XB = C::XB, SB = C::SB;
-  constexpr int APS = kSkKS / KA;                          // A-stages per unit
-  constexpr int WW = KA / 2;                               // bf16 pairs per row and A-stage
-  constexpr uint32_t IDESC = idesc_bf16_f32(128, BN);
-  constexpr uint32_t A_COL0 = MG * ACC;                    // first TMEM column of the A slots
-  constexpr int GW = C::GW, PPW = C::PPW;
-  constexpr int kTma = GW * MG, kEpi0 = GW * MG + 1;
-  static_assert(C::ok, "TMEM budget / A-stage split");
-
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int S = p.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB);
-  uint64_t* empty = full + S;
-  uint64_t* a_empty = empty + S;                           // [MG][SAG]: the slot's MMAs completed
-  uint64_t* acc_full = a_empty + MG * SAG;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
-
-  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);   // provably warp-uniform
-  const int lane = threadIdx.x & 31;
-  const int cta = blockIdx.x;
-  const int u0 = sk_unit0(p, cta);
-  const int u1 = u0 + p.units_base + (cta < p.units_rem ? 1 : 0);
-  const int upt = p.upt;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MG);                            // one MMA commit per masker group
-    }
-    for (int s = 0; s < MG * SAG; ++s) mbar_init(&a_empty[s], 1);
-    mbar_init(acc_full, MG);
-    mbar_init(acc_empty, 4);
-    mbar_fence_init();
-  }
-  if (warp == 0) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_launch_dependents();
-#ifdef MGLU_SK_TRACE
-  __shared__ long long t0s;
-  __shared__ int sk_trace_on;
-  if (threadIdx.x == 0) {
-    t0s = clock64();
-    sk_trace_on = cta == 0 ? (atomicAdd(&g_skcall, 1u) == 20u) : 0;
-    if (cta == 0 && sk_trace_on) for (int e = 0; e < 8; ++e) for (int i = 0; i < 256; ++i) g_sktrace[e][i] = 0;
-  }
-  __syncthreads();
-#define SKT(ev, idx) do { if (cta == 0 && lane == 0 && sk_trace_on && (idx) < 256) g_sktrace[ev][idx] = (uint32_t)(clock64() - t0s) | 1u; } while (0)
-#else
-#define SKT(ev, idx) do {} while (0)
-#endif
-
-  if (warp == kTma) {
-    // ------------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      prefetch_tmap(&mW);
-      prefetch_tmap(&mC);
-      prefetch_tmap(&mX);
-      const uint64_t pol = policy_evict_first();
-      const int n = u1 - u0;
-      const int pre = n < S ? n : S;
-      // W and the codes of the first `pre` stages before the predecessor finishes (constants) ...
-      for (int i = 0; i < pre; ++i) {
-        const int u = u0 + i, tile = u / upt, ks = u - tile * upt;
-        uint8_t* st = smem + (size_t)i * SB;
-        mbar_arrive_expect_tx(&full[i], (uint32_t)(WB + (MGLU_SK_NOX ? 0 : XB) + C::CB));
-        tma_load_3d_hint(st, &mW, 0, tile * 128, ks * (kSkKS / 64), &full[i], pol);
-        tma_load_2d_hint(st + WB + XB, &mC, (ks * WPS) / CW * CW, tile * 128, &full[i], pol);
-      }
-      pdl_wait();                                          // ... x only after it
-      for (int i = 0; i < pre; ++i) {
-        const int ks = (u0 + i) % upt;
-        if (!MGLU_SK_NOX) tma_load_3d(smem + (size_t)i * SB + WB, &mX, 0, 0, ks * (kSkKS / 64), &full[i]);
-      }
-      int s = pre % S;
-      uint32_t ph = pre == S ? 1u : 0u;
-      for (int i = pre; i < n; ++i) {
-        const int u = u0 + i, tile = u / upt, ks = u - tile * upt;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* st = smem + (size_t)s * SB;
-        mbar_arrive_expect_tx(&full[s], (uint32_t)(WB + (MGLU_SK_NOX ? 0 : XB) + C::CB));
-        tma_load_3d_hint(st, &mW, 0, tile * 128, ks * (kSkKS / 64), &full[s], pol);
-        if (!MGLU_SK_NOX) tma_load_3d(st + WB, &mX, 0, 0, ks * (kSkKS / 64), &full[s]);
-        tma_load_2d_hint(st + WB + XB, &mC, (ks * WPS) / CW * CW, tile * 128, &full[s], pol);
-        if (++s == S) { s = 0; ph ^= 1; }
-      }
-    }
-  } else if (warp < GW * MG) {
-    // ------------------------------------------------------------------ masker + MMA issue
-    const int g = warp / GW;                               // A-stages js = g (mod MG)
-    const int wg = warp - g * GW;                          // warp within the group
-    const int part = wg >> 2;                              // which PPW pairs of the A-stage
-    const int m = (warp & 3) * 32 + lane;                  // tile row = TMEM lane (warp's lane quarter)
-    const bool leader_warp = wg == 0;
-    const uint32_t a_lane = tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL0 + (uint32_t)(g * SAG * SLOT);
-    const uint32_t a_all = tmem + A_COL0 + (uint32_t)(g * SAG * SLOT);   // lane 0: the MMA's view
-    const uint32_t dacc = tmem + (uint32_t)(g * ACC);
-    int s = 0, jg = 0;
-    uint32_t ph = 0, acc_uses = 0;
-    bool fresh = true;                                     // next MMA starts a segment (accumulate = 0)
-    for (int u = u0; u < u1; ++u) {
-      const int ks = u % upt;
-      const bool seg_first = u == u0 || ks == 0;
-      const bool seg_last = u == u1 - 1 || ks == upt - 1;
-      if (seg_first) fresh = true;
-      mbar_wait(&full[s], ph);
-      if (warp == 0) SKT(1, u - u0);
-      const uint8_t* st = smem + (size_t)s * SB;
-      const uint32_t st_addr = smem_u32(st);
-      const int wofs = (ks * WPS) % CW;                    // first word of this unit in the code box
-#pragma unroll
-      for (int a = g; a < APS; a += MG) {
-        const int col = a * KA + part * 2 * PPW;           // first column of this warp's pairs in the unit
-        uint32_t w[PPW];
-#pragma unroll
-        for (int c = 0; c < PPW / 4; ++c) {
-          const uint32_t chunk = (uint32_t)(((col & 63) >> 3) + c) ^ (uint32_t)(m & 7);
-          const uint4 v = *reinterpret_cast<const uint4*>(st + (col >> 6) * 16384 + m * 128 + chunk * 16);
-          w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
-        }
-        // mask words: NG 32-column groups covered by this warp's pairs, n_m words each
-        constexpr int NG = PPW > 16 ? PPW / 16 : 1, PPG = PPW > 16 ? 16 : PPW;
-        uint32_t cw[NG][NM];
-#pragma unroll
-        for (int gi = 0; gi < NG; ++gi) {
-          const uint8_t* crow = st + WB + XB + m * CW * 4 + (wofs + ((col >> 5) + gi) * NM) * 4;
-          if constexpr (NM == 1) cw[gi][0] = *reinterpret_cast<const uint32_t*>(crow);
-          else if constexpr (NM == 2) { const uint2 v = *reinterpret_cast<const uint2*>(crow); cw[gi][0] = v.x; cw[gi][1] = v.y; }
-          else {
-#pragma unroll
-            for (int q = 0; q < NM / 4; ++q) {
-              const uint4 v = *reinterpret_cast<const uint4*>(crow + 16 * q);
-              cw[gi][4 * q] = v.x; cw[gi][4 * q + 1] = v.y; cw[gi][4 * q + 2] = v.z; cw[gi][4 * q + 3] = v.w;
-            }
-          }
-        }
-        const int pair0 = (col & 31) >> 1;                 // first pair of this warp's range in its 32-column group
-        const int sa = jg % SAG;
-        mbar_wait(&a_empty[g * SAG + sa], ((uint32_t)(jg / SAG) & 1u) ^ 1u);   // slot's previous MMAs done
-        if (warp == 0) SKT(2, jg);
-        tc_fence_after();
-        const uint32_t a0 = a_lane + (uint32_t)(sa * SLOT + part * PPW);
-        if (MGLU_SK_ABL != 2) tmem_st_n<PPW>(a0, w);       // operand 0: W itself (for t)
-#pragma unroll
-        for (int i = 0; i < NM; ++i) {
-          uint32_t op[PPW];
-#pragma unroll
-          for (int gi = 0; gi < NG; ++gi)
-#pragma unroll
-            for (int q = 0; q < PPG; ++q)                  // pair pair0 + q of group gi: bits (pair, pair + 16)
-              op[gi * PPG + q] = MGLU_SK_ABL == 3 ? w[gi * PPG + q] : sign_flip(w[gi * PPG + q], cw[gi][i], 1u << (15 - pair0 - q));
-          if (MGLU_SK_ABL != 2) tmem_st_n<PPW>(a0 + (uint32_t)((1 + i) * WW), op);
-          else if (op[0] == 0x12345u && op[PPW - 1] == 0x777u) asm volatile("trap;");   // keep the math
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        named_bar_sync(1 + g, 32 * GW);                    // the group's slot is complete
-        const bool last_in_unit = a + MG >= APS;
-        if (leader_warp) {
-          tc_fence_after();
-          if (fresh && acc_uses > 0) {                     // the epilogue still reads the previous segment
-            mbar_wait(acc_empty, (acc_uses - 1) & 1u);
-            tc_fence_after();
-          }
-          if (elect_one()) {
-            const int colA = a * KA;
-#pragma unroll
-            for (int kk = 0; kk < KA / 16; ++kk) {
-              const int k16 = (colA >> 4) + kk;            // k16 step within the unit
-              const uint64_t bdesc = smem_desc_kmajor(st_addr + WB + (k16 >> 2) * BN * 128, 128) + (uint64_t)((k16 & 3) * 2);
-              const uint32_t accum = (fresh && kk == 0) ? 0u : 1u;
-              const uint32_t asl = a_all + (uint32_t)(sa * SLOT + kk * 8);
-#pragma unroll
-              for (int o = 0; o < NOP; ++o)                // t += x W, u_i += x (sigma_i W)
-                if (MGLU_SK_ABL == 0 || MGLU_SK_ABL == 3) tc_mma_ts(dacc + (uint32_t)(o * BN), asl + (uint32_t)(o * WW), bdesc, IDESC, accum);
-            }
-            tc_commit(&a_empty[g * SAG + sa]);
-            if (last_in_unit) tc_commit(&empty[s]);        // x (and this group's reads) done with the stage
-            if (last_in_unit && seg_last) tc_commit(acc_full);
-          }
-          __syncwarp();
-          if (g == 0) SKT(3, jg); else SKT(7, jg);
-        }
-        fresh = false;
-        ++jg;
-      }
-      if (seg_last) ++acc_uses;
-      if (++s == S) { s = 0; ph ^= 1; }
-    }
-  } else if (warp >= kEpi0) {
-    // ------------------------------------------------------------------ epilogue
-    const int quarter = warp & 3;
-    const int m = quarter * 32 + lane;                     // tile row = TMEM lane
-    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-    const int B = p.B;
-    constexpr int CH = 4;                                  // tokens per epilogue chunk
-    const int nch = (B + CH - 1) / CH;
-    pdl_wait();                                            // ws / flags / out belong to the predecessor until now
-    uint32_t acc_uses = 0;
-    int u = u0;
-    while (u < u1) {
-      const int tile = u / upt;
-      const int tile_end = (tile + 1) * upt;
-      const int seg_end = u1 < tile_end ? u1 : tile_end;
-      const bool owner = u == tile * upt;
-      const bool whole = owner && seg_end == tile_end;
-      mbar_wait(acc_full, acc_uses & 1u);
-      SKT(6, acc_uses);
-      tc_fence_after();
-      const int grow = tile * 128 + m;
-      int ncon = 0;
-      if (owner && !whole) {
-        // the contributors are the following CTAs whose first unit lies inside this tile
-        while (cta + 1 + ncon < (int)gridDim.x && sk_unit0(p, cta + 1 + ncon) < tile_end) ++ncon;
-        for (int k = 1; k <= ncon; ++k) {
-          uint32_t polls = 0;
-          while (ld_acquire_u32(p.flags + cta + k) == 0u) {
-            if (++polls == (1u << 26)) __trap();
-            __nanosleep(64);
-          }
-        }
-      }
-      for (int ch = 0; ch < nch; ++ch) {
-        float f[NOP][CH];
-#pragma unroll
-        for (int o = 0; o < NOP; ++o) {
-          uint32_t v[MG][CH];
-#pragma unroll
-          for (int gg = 0; gg < MG; ++gg) tmem_ld4(lane_base + (uint32_t)(gg * ACC + o * BN + ch * CH), v[gg]);
-          tmem_ld_wait();
-#pragma unroll
-          for (int q = 0; q < CH; ++q) {                    // group accumulators, summed in group order
-            f[o][q] = __uint_as_float(v[0][q]);
-#pragma unroll
-            for (int gg = 1; gg < MG; ++gg) f[o][q] += __uint_as_float(v[gg][q]);
-          }
-        }
-        if (!owner) {
-          // contributor: publish the partial accumulators of this (first) segment
-          float* wsp = p.ws + (size_t)cta * NOP * B * 128 + m;
-#pragma unroll
-          for (int o = 0; o < NOP; ++o)
-#pragma unroll
-            for (int q = 0; q < CH; ++q) {
-              const int tok = ch * CH + q;
-              if (tok < B) __stcg(wsp + ((size_t)o * B + tok) * 128, f[o][q]);
-            }
-          continue;
-        }
-        for (int k = 1; k <= ncon; ++k) {                  // fixed order: own, then CTA + 1, + 2, ...
-          const float* wsp = p.ws + (size_t)(cta + k) * NOP * B * 128 + m;
-#pragma unroll
-          for (int o = 0; o < NOP; ++o)
-#pragma unroll
-            for (int q = 0; q < CH; ++q) {
-              const int tok = ch * CH + q;
-              if (tok < B) f[o][q] += __ldcg(wsp + ((size_t)o * B + tok) * 128);
-            }
-        }
-        if (grow < p.h) {
-#pragma unroll
-          for (int q = 0; q < CH; ++q) {
-            const int tok = ch * CH + q;
-            if (tok < B) {
-              const float t = f[0][q];
-              float y = 0.f;
-#pragma unroll
-              for (int i = 0; i < NM; ++i) {
-                const float sg = 0.5f * (t + f[1 + i][q]);                   // s_i = (t + u_i) / 2
-                y = fmaf(act_rt(p.act, sg), t - sg, y);                        // g(s_i) (t - s_i)
-              }
-              p.out[(size_t)tok * p.h + grow] = __float2bfloat16_rn(y);
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);               // accumulators free for the next segment
-      if (!owner) {
-        __threadfence();
-        named_bar_sync(15, 128);
-        if (warp == kEpi0 && lane == 0) st_release_u32(p.flags + cta, 1u);
-      } else if (ncon) {
-        named_bar_sync(15, 128);                           // every epilogue thread has read the partials
-        if (warp == kEpi0)
-          for (int k = lane; k < ncon; k += 32) p.flags[cta + 1 + k] = 0u;   // re-arm for the next call
-      }
-      ++acc_uses;
-      u = seg_end;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-#ifdef MGLU_SK_TRACE
-  if (cta == 0 && threadIdx.x == 0 && sk_trace_on) {
-    for (int e = 0; e < 8; ++e)
-      for (int i = 0; i < 256; ++i)
-        if (g_sktrace[e][i]) printf("SKT %d %d %u\n", e, i, g_sktrace[e][i]);
-  }
-#endif
-  if (warp == 0) tmem_dealloc(tmem, 512);
-}
-
-// ---------------------------------------------------------------------------------------------
-// Variant 1: a dedicated MMA warp and ONE shared accumulator set (double-buffered when it fits):
-// masker groups arrive on a per-slot a_full, the MMA warp waits it and issues all (n_m + 1) TS MMAs
-// of the A-stage (W itself is operand 0 in the slot, so no MMA reads A from shared memory).
-template <int NM, int BN, int MG> struct Sk1Cfg {
+// geometry of one instantiation: NM masks, BN token columns, MG masker groups of 4 warps
+template <int NM, int BN, int MG> struct SkCfg {
   static constexpr int NOP = NM + 1;
   static constexpr int KA = NM == 8 ? 16 : MGLU_SK_KA;
   static constexpr int SLOT = NOP * KA / 2;
@@ -453,10 +104,10 @@ template <int NM, int BN, int MG> struct Sk1Cfg {
 };
 
 template <int NM, int BN, int MG>
-__global__ void __launch_bounds__(Sk1Cfg<NM, BN, MG>::THREADS, 1)
-gemv_tc1_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const __grid_constant__ CUtensorMap mX,
+__global__ void __launch_bounds__(SkCfg<NM, BN, MG>::THREADS, 1)
+gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const __grid_constant__ CUtensorMap mX,
                 const __grid_constant__ CUtensorMap mC) {
-  using C = Sk1Cfg<NM, BN, MG>;
+  using C = SkCfg<NM, BN, MG>;
   constexpr int NOP = C::NOP, KA = C::KA, SLOT = C::SLOT, SA = C::SA, NACC = C::NACC, ACC = C::ACC;
   constexpr int WPS = C::WPS, CW = C::CW, WB = C::WB, XB = C::XB, SB = C::SB;
   constexpr int APS = kSkKS / KA, WW = KA / 2;

@@ -400,12 +400,6 @@ cudaError_t tc_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const 
 // ------------------------------------------------------------------ tcgen05 stream-K decode dispatch
 constexpr int kSkMaxB = 64;
 constexpr int kAutoMmaMaxB = 4, kAutoSkMaxB = 24;
-#ifndef MGLU_SK_MG
-#define MGLU_SK_MG 2
-#endif
-#ifndef MGLU_SK_IMPL
-#define MGLU_SK_IMPL 1   // 1: dedicated MMA warp, shared accumulators; 2: groups issue their own MMAs
-#endif
 
 bool sk_can_serve(const mglu_ctx* hd, int64_t B) {
   // 64-column units; mask-word rows of d/32 * n_m u32 words must be 16-byte multiples (TMA)
@@ -428,10 +422,10 @@ cudaError_t sk_alloc(mglu_ctx* hd) {
   return e;
 }
 
-template <int NM, int BN, int MG, int WQ, int IMPL>
+template <int NM, int BN, int MG>
 cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
                       cudaStream_t st) {
-  using C = typename std::conditional<IMPL == 1, mglu::Sk1Cfg<NM, BN, MG>, mglu::SkCfg<NM, BN, MG, WQ>>::type;
+  using C = mglu::SkCfg<NM, BN, MG>;
   CUtensorMap mW, mX, mC;
   const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
   constexpr int KB = mglu::kSkKS / 64;
@@ -459,28 +453,18 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   const int S = (int)std::min<size_t>(16, (cap - fixed) / C::SB);
   p.stages = S;
   const size_t smem = (size_t)S * C::SB + fixed;
-  auto launch = [&](auto kern) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    return launch_pdl(kern, dim3((unsigned)G), dim3(C::THREADS), smem, st, p, mW, mX, mC);
-  };
-  if constexpr (IMPL == 1) return launch(mglu::gemv_tc1_kernel<NM, BN, MG>);
-  else return launch(mglu::gemv_tc_kernel<NM, BN, MG, WQ>);
+  auto kern = mglu::gemv_tc_kernel<NM, BN, MG>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(kern, dim3((unsigned)G), dim3(C::THREADS), smem, st, p, mW, mX, mC);
 }
 
-// masker organisation: MGLU_SK_MG groups x MGLU_SK_WQ warps per lane quarter when the TMEM budget
-// allows (accumulators are per group, >= 2 A slots per group), else fewer groups
+// two masker groups when the TMEM budget allows, else one
 template <int NM, int BN>
 cudaError_t run_sk_mg(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
                       cudaStream_t st) {
-#if MGLU_SK_IMPL == 1
-  if constexpr (mglu::Sk1Cfg<NM, BN, 2>::ok) return run_sk_bn<NM, BN, 2, 1, 1>(hd, x, B, Wt, codes, out, st);
-  else return run_sk_bn<NM, BN, 1, 1, 1>(hd, x, B, Wt, codes, out, st);
-#else
-  if constexpr (mglu::SkCfg<NM, BN, MGLU_SK_MG, MGLU_SK_WQ>::ok)
-    return run_sk_bn<NM, BN, MGLU_SK_MG, MGLU_SK_WQ, 2>(hd, x, B, Wt, codes, out, st);
-  else return run_sk_bn<NM, BN, 1, MGLU_SK_WQ, 2>(hd, x, B, Wt, codes, out, st);
-#endif
+  if constexpr (mglu::SkCfg<NM, BN, 2>::ok) return run_sk_bn<NM, BN, 2>(hd, x, B, Wt, codes, out, st);
+  else return run_sk_bn<NM, BN, 1>(hd, x, B, Wt, codes, out, st);
 }
 
 template <int NM>
