@@ -31,7 +31,10 @@ namespace mglu {
 template <int NM> struct TcCfg;
 template <> struct TcCfg<1> { static constexpr int BN = 224, KA = 32, MPC = 1; };
 template <> struct TcCfg<2> { static constexpr int BN = 128, KA = 32, MPC = 2; };
-template <> struct TcCfg<4> { static constexpr int BN = 64, KA = 32, MPC = 4; };
+#ifndef MGLU_TC_KA4
+#define MGLU_TC_KA4 32
+#endif
+template <> struct TcCfg<4> { static constexpr int BN = 64, KA = MGLU_TC_KA4, MPC = 4; };
 template <> struct TcCfg<8> { static constexpr int BN = 64, KA = 32, MPC = 4; };
 
 constexpr int kTcThreads = 320;
@@ -179,7 +182,6 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t a_lane = tmem + lane_off + A_COL0;
     const uint32_t wrow_off = (uint32_t)(XB + m * 128);    // row m of the W tile (128-byte rows)
-    const uint32_t crow_off = (uint32_t)(XB + WB + m * CW * 4);
     int s = 0;
     uint32_t ph = 0;
     int js = 0;
@@ -200,9 +202,8 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
         uint32_t cw[MPC];
         const int grp = (a * KA) >> 5;                     // code group within the stage
         const int wofs = (ks * 2 * NM) % CW;               // stage's first word within the loaded box
-#pragma unroll
-        for (int i = 0; i < MPC; ++i)
-          cw[i] = *reinterpret_cast<const uint32_t*>(st + crow_off + (wofs + grp * NM + moff + i) * 4);
+        // the code box is swizzled like its row width (bank-conflict-free 16-byte reads)
+        lds_words_swz<MPC>(st + XB + WB, (uint32_t)(m * CW * 4 + (wofs + grp * NM + moff) * 4), CW * 4, cw);
         const int pair0 = (a * KA) & 31 ? 8 : 0;           // first pair of the A-stage in its group
         uint32_t op[NOP][WW];
 #pragma unroll

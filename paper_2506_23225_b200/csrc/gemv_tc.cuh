@@ -240,17 +240,8 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
           const uint4 v = *reinterpret_cast<const uint4*>(st + (col >> 6) * 16384 + m * 128 + chunk * 16);
           w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
         }
-        uint32_t cw[NM];
-        const uint8_t* crow = st + WB + XB + m * CW * 4 + (wofs + (col >> 5) * NM) * 4;
-        if constexpr (NM == 1) cw[0] = *reinterpret_cast<const uint32_t*>(crow);
-        else if constexpr (NM == 2) { const uint2 v = *reinterpret_cast<const uint2*>(crow); cw[0] = v.x; cw[1] = v.y; }
-        else {
-#pragma unroll
-          for (int q = 0; q < NM / 4; ++q) {
-            const uint4 v = *reinterpret_cast<const uint4*>(crow + 16 * q);
-            cw[4 * q] = v.x; cw[4 * q + 1] = v.y; cw[4 * q + 2] = v.z; cw[4 * q + 3] = v.w;
-          }
-        }
+        uint32_t cw[NM];                                   // (swizzled code box: conflict-free reads)
+        lds_words_swz<NM>(st + WB + XB, (uint32_t)(m * CW * 4 + (wofs + (col >> 5) * NM) * 4), CW * 4, cw);
         const int pair0 = (col & 31) >> 1;
         const int sa = js % SA;
         mbar_wait(&a_empty[sa], ((uint32_t)(js / SA) & 1u) ^ 1u);

@@ -308,8 +308,19 @@ bool encode_2d_bf16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t ro
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// 2-D row-major [rows][cols] u32 tensor, box [brows][bcols], no swizzle
-bool encode_2d_u32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t bcols, uint32_t brows) {
+// TMA swizzle of a code box with rb-byte rows (the kernels read it through lds_words_swz)
+CUtensorMapSwizzle code_swizzle(int rb) {
+  switch (mglu::code_swizzle_bytes(rb)) {
+    case 128: return CU_TENSOR_MAP_SWIZZLE_128B;
+    case 64: return CU_TENSOR_MAP_SWIZZLE_64B;
+    case 32: return CU_TENSOR_MAP_SWIZZLE_32B;
+    default: return CU_TENSOR_MAP_SWIZZLE_NONE;
+  }
+}
+
+// 2-D row-major [rows][cols] u32 tensor, box [brows][bcols]
+bool encode_2d_u32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t bcols, uint32_t brows,
+                   CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   EncodeTiledFn enc = get_encoder();
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};
@@ -317,7 +328,7 @@ bool encode_2d_u32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t row
   cuuint32_t box[2] = {bcols, brows};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -328,7 +339,8 @@ cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
   if (!encode_2d_bf16(&mX, x, hd->d, B, mglu::kTcK, BN, sw) ||
       !encode_2d_bf16(&mW, Wt, hd->d, hd->h, mglu::kTcK, 128, sw) ||
-      !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, mglu::tc_code_words<NM>(), 128))
+      !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, mglu::tc_code_words<NM>(), 128,
+                     code_swizzle(mglu::tc_code_words<NM>() * 4)))
     return cudaErrorInvalidValue;
   mglu::TcParams p;
   p.out = (__nv_bfloat16*)out;
@@ -431,7 +443,7 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   constexpr int KB = mglu::kSkKS / 64;
   if (!encode_3d_blocks(&mW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, 128, KB, sw) ||
       !encode_3d_blocks(&mX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, hd->d, B, 64, BN, KB, sw) ||
-      !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, C::CW, 128))
+      !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, C::CW, 128, code_swizzle(C::CW * 4)))
     return cudaErrorInvalidValue;
   mglu::SkParams p;
   p.out = (__nv_bfloat16*)out;

@@ -76,6 +76,27 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// N consecutive u32 mask words starting at byte `lin` of a TMA box whose rows are `rb` bytes,
+// loaded with the swizzle code_swizzle_bytes(rb) (32/64/128-byte rows: that swizzle, else none):
+// 16-byte chunk c of a 1024-byte-aligned region lands at chunk c ^ ((lin >> 7) & (rb / 16 - 1)).
+// The words of one chunk keep their order, so each chunk is one vector load.
+__host__ __device__ constexpr int code_swizzle_bytes(int rb) { return rb == 128 ? 128 : rb == 64 ? 64 : rb == 32 ? 32 : 0; }
+template <int N>
+__device__ __forceinline__ void lds_words_swz(const uint8_t* base, uint32_t lin, uint32_t rb, uint32_t (&w)[N]) {
+  const uint32_t sw = (uint32_t)code_swizzle_bytes((int)rb);
+  const uint32_t mask = sw ? sw / 16 - 1 : 0;
+  auto at = [&](uint32_t l) { return base + (l ^ (((l >> 7) & mask) << 4)); };
+  if constexpr (N == 1) w[0] = *reinterpret_cast<const uint32_t*>(at(lin));
+  else if constexpr (N == 2) { const uint2 v = *reinterpret_cast<const uint2*>(at(lin)); w[0] = v.x; w[1] = v.y; }
+  else {
+#pragma unroll
+    for (int q = 0; q < N / 4; ++q) {
+      const uint4 v = *reinterpret_cast<const uint4*>(at(lin + 16 * q));
+      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
+  }
+}
+
 // named barrier over a subset of warps
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
