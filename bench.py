@@ -363,25 +363,49 @@ def run_mglu(args, ws, rank, local):
     else:
         peak, peak_src, bound = peaks["hbm_gbs"], "hbm_gbs (copy)", "hbm"
 
-    # e2e through the C-ABI host-buffer entry: x H2D + kernel + y D2H every step
-    xh = x.cpu().pin_memory()
-    yh = torch.empty(B, h_loc, dtype=torch.bfloat16).pin_memory()
+    # e2e through the C-ABI host-buffer entry: x H2D + kernel + y D2H every step.  Consecutive
+    # steps alternate over E streams, each with its own handle (own device staging buffers) and its
+    # own pinned host buffers, so one step's copies overlap another step's kernel; the timed region
+    # spans every stream (start event joined by all, end after all have drained).
+    E = max(1, args.e2e_streams)
+    e_layers = [layer] + [Mglu(d, h_loc, n_m, act=act, dtype="bf16", device=local, path=args.path) for _ in range(E - 1)]
+    e_streams = [stream] + [torch.cuda.Stream() for _ in range(E - 1)]
+    xh = [x.cpu().pin_memory() for _ in range(E)]
+    yh = [torch.empty(B, h_loc, dtype=torch.bfloat16).pin_memory() for _ in range(E)]
 
     def step_host(k):
         Wt, codes = layers[k % L]
-        layer.forward_host(xh, Wt, codes, yh, stream=stream)
+        e = k % E
+        e_layers[e].forward_host(xh[e], Wt, codes, yh[e], stream=e_streams[e])
 
-    with torch.cuda.stream(stream):
-        for k in range(max(3, args.warmup)):
+    def time_e2e(K):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for st_ in e_streams[1:]:
+            st_.wait_event(ev0)
+        for k in range(K):
             step_host(k)
-        stream.synchronize()
-        barrier(ws)
-        el_e2e = time_steps(step_host, args.steps, stream)
-        barrier(ws)
+        for st_ in e_streams[1:]:
+            stream.wait_stream(st_)
+        ev1.record(stream)
+        ev1.synchronize()
+        return ev0.elapsed_time(ev1) / 1e3
+
+    for k in range(max(3, args.warmup)):
+        step_host(k)
+    torch.cuda.synchronize()
+    barrier(ws)
+    el_e2e = time_e2e(args.steps)
+    barrier(ws)
     el_e2e = max_over_ranks(ws, el_e2e)
     e2e = {"value": units_layer * args.steps / el_e2e / scale, "unit": unit,
            "h2d_bytes_per_step": B * d * 2 * ws, "d2h_bytes_per_step": B * h * 2,
-           "us_per_call": el_e2e / args.steps * 1e6}
+           "us_per_call": el_e2e / args.steps * 1e6, "streams": E,
+           "how": "mglu_forward_host per step (pinned x -> device, forward, y -> pinned host), steps alternating over "
+                  f"{E} streams/handles so copies overlap kernels"}
+    for extra in e_layers[1:]:
+        extra.close()
 
     out = None
     if rank == 0:
@@ -435,6 +459,7 @@ def main(argv=None):
     ap.add_argument("--layers", type=int, default=4, help="distinct layer copies rotated (L2 hygiene)")
     ap.add_argument("--clock-window", type=float, default=0.3)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--e2e-streams", type=int, default=2, help="streams the e2e (host-buffer) leg alternates over")
     ap.add_argument("--no-comparator", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shape", default=None, help="experiment: d,h,n_m,B (overrides --workload)")
