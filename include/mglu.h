@@ -121,6 +121,24 @@ mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* W
 mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, const void* Wt,
                                   const void* packed, float* z, void* stream);
 
+/* Top-K routed MGLU (Appendix B).
+ * mglu_router_topk: router logits l[b] = x[b] W_r in fp32 from bf16 inputs, then
+ *   G[b] = Softmax(TopK(l[b])): the K largest logits (ties -> lowest index) get the
+ *   softmax weights over those K values, every other entry exactly 0.
+ *   Wr [n_m][d] bf16 row-major (row i = logit i's weights, like Wt), device; G [B][n_m] fp32,
+ *   device, written.  1 <= K <= n_m.  bf16 handles only.  One launch.
+ *   Errors: INVALID_ARG (nulls, B < 0, K out of range), MISALIGNED, UNSUPPORTED (fp32), CUDA.
+ * mglu_forward_routed: y[b][j] = sum_i G[b][i] g(s_i) (t - s_i) in one pass over W and
+ *   the codes, G [B][n_m] fp32 on the device (e.g. from mglu_router_topk on the same stream; read
+ *   after the predecessor completes).  Masks whose weight is 0 for every token of the call are not
+ *   evaluated (MMA path: their sign flips and MMAs are skipped).  Runs the MMA path (bf16,
+ *   B <= 8) or the SIMT path; forcing TCGEN05/TCDEC returns UNSUPPORTED in this version.
+ *   Errors as mglu_forward, plus INVALID_ARG / MISALIGNED for G. */
+mglu_status mglu_router_topk(mglu_handle hd, const void* x, int64_t B, const void* Wr, int K, float* G,
+                             void* stream);
+mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* packed,
+                                const float* G, void* out, void* stream);
+
 /* End-to-end form: x_host [B][d] and out_host [B][h] are HOST buffers (pinned for async
  * copies; pageable works but serialises).  Copies x to the handle's device staging buffer,
  * runs mglu_forward, copies y back, all enqueued on `stream` (the caller synchronises).  The

@@ -32,6 +32,17 @@ __device__ __forceinline__ float mglu_epilogue(float t, const float (&s)[NM]) {
   return y;
 }
 
+// Top-K routed epilogue (Appendix B): y = sum_i G_i g(s_i) (t - s_i); gw == nullptr is
+// the plain Eq. 3 (every G_i = 1)
+template <int ACT, int NM>
+__device__ __forceinline__ float mglu_epilogue_w(float t, const float (&s)[NM], const float* gw) {
+  if (!gw) return mglu_epilogue<ACT, NM>(t, s);
+  float y = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NM; ++i) y = fmaf(gw[i] * act_g<ACT>(s[i]), t - s[i], y);
+  return y;
+}
+
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 

@@ -56,6 +56,7 @@ __host__ __device__ constexpr int dec_wpt(int tiles) { return kDecConsumers / ti
 struct DecParams {
   const __nv_bfloat16* x;
   __nv_bfloat16* out;
+  const float* G;            // Top-K routed gate weights [B][n_m] (nullptr: plain Eq. 3)
   int B, d, h;
   int rows_base, rows_rem;   // CTA c owns rows_base + (c < rows_rem) rows
   int stages;                // ring depth
@@ -160,6 +161,13 @@ gemv_mma_kernel(const DecParams p,
       xs[(size_t)(2 * b + (q & 1)) * p.xpar + (q >> 1)] = val;
     }
   }
+  // routed forward: masks with zero weight for every token of the batch are skipped entirely
+  // (their HMMAs and sign flips; uniform across the CTA)
+  uint32_t active = (1u << NM) - 1u;
+  if (p.G) {
+    active = 0u;
+    for (int q = 0; q < B * NM; ++q) active |= (p.G[q] != 0.0f ? 1u : 0u) << (q % NM);
+  }
   named_bar_sync(1, kDecConsumers * 32);
 
   float acc[NB][NM + 1][4];
@@ -233,6 +241,7 @@ gemv_mma_kernel(const DecParams p,
           // u_i += x (sigma_i (.) W): pair q of the thread's 8 columns is register q of the quad
 #pragma unroll
           for (int ii = 0; ii < NM; ++ii) {
+            if (!((active >> ii) & 1u)) continue;
             const uint32_t a0 = sign_flip(wq.x, mw[ii], mul[0]), a1 = sign_flip(wq.y, mw[ii], mul[1]);
             const uint32_t a2 = sign_flip(wq.z, mw[ii], mul[2]), a3 = sign_flip(wq.w, mw[ii], mul[3]);
 #pragma unroll
@@ -281,7 +290,7 @@ gemv_mma_kernel(const DecParams p,
           float sv[NM];
 #pragma unroll
           for (int ii = 0; ii < NM; ++ii) sv[ii] = 0.5f * (v[nb][0] + v[nb][1 + ii]);   // s_i = (t + u_i) / 2
-          const float y = mglu_epilogue<ACT, NM>(v[nb][0], sv);       // Eq. 3, value = t - s_i
+          const float y = mglu_epilogue_w<ACT, NM>(v[nb][0], sv, p.G ? p.G + (size_t)tok * NM : nullptr);   // Eq. 3 / routed
           p.out[(size_t)tok * p.h + r0 + row] = __float2bfloat16_rn(y);
         }
       }

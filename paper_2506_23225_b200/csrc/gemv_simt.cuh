@@ -54,7 +54,7 @@ template <typename T, int NM, int ACT, bool PARTIALS>
 __global__ void __launch_bounds__(256)
 gemv_simt_kernel(const T* __restrict__ x, int B, int d, const T* __restrict__ Wt,
                  const uint8_t* __restrict__ codes, int h, T* __restrict__ out,
-                 float* __restrict__ z) {
+                 float* __restrict__ z, const float* __restrict__ G) {
   pdl_wait();
   const int lane = threadIdx.x & 31;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
@@ -116,7 +116,8 @@ gemv_simt_kernel(const T* __restrict__ x, int B, int d, const T* __restrict__ Wt
                 zb[(size_t)(NM + i) * h + j] = t[b] - s[b][i]; // z[n_m+i]  = t - s_i
               }
             } else {
-              IoT<T>::store(out + (size_t)(b0 + b) * h + j, mglu_epilogue<ACT, NM>(t[b], s[b]));
+              IoT<T>::store(out + (size_t)(b0 + b) * h + j,
+                            mglu_epilogue_w<ACT, NM>(t[b], s[b], G ? G + (size_t)(b0 + b) * NM : nullptr));
             }
           }
         }

@@ -22,6 +22,7 @@
 #include "gemm_tc.cuh"
 #include "gemv_tc.cuh"
 #include "pack.cuh"
+#include "router.cuh"
 
 struct mglu_ctx {
   int64_t d = 0, h = 0;
@@ -56,6 +57,10 @@ struct mglu_ctx {
 };
 
 namespace {
+
+// gate weights of the routed forward being enqueued by this host thread (nullptr: plain forward);
+// set and cleared by mglu_forward_routed around the regular dispatch
+thread_local const float* t_routed_G = nullptr;
 
 const char* kStatusStr[] = {"MGLU_OK", "MGLU_ERR_INVALID_ARG", "MGLU_ERR_UNSUPPORTED",
                             "MGLU_ERR_MISALIGNED", "MGLU_ERR_CUDA", "MGLU_ERR_OOM"};
@@ -108,7 +113,7 @@ cudaError_t run_simt(mglu_ctx* hd, const void* x, int B, const void* Wt, const v
   if (blocks > cap) blocks = cap;
   return launch_pdl(mglu::gemv_simt_kernel<T, NM, ACT, PARTIALS>, dim3((unsigned)blocks),
                     dim3(warps_per_block * 32), 0, st, (const T*)x, B, (int)hd->d, (const T*)Wt,
-                    (const uint8_t*)codes, (int)hd->h, (T*)out, z);
+                    (const uint8_t*)codes, (int)hd->h, (T*)out, z, t_routed_G);
 }
 
 template <typename T, bool PARTIALS, int NM>
@@ -221,6 +226,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   mglu::DecParams p;
   p.x = (const __nv_bfloat16*)x;
   p.out = (__nv_bfloat16*)out;
+  p.G = t_routed_G;
   p.B = B;
   p.d = (int)hd->d;
   p.h = (int)hd->h;
@@ -618,17 +624,16 @@ mglu_status mglu_set_path(mglu_handle hd, int path) {
 int mglu_last_launch_count(mglu_handle hd) { return hd ? hd->last_launches : -1; }
 int mglu_last_path(mglu_handle hd) { return hd ? hd->last_path : -1; }
 
-mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* Wt,
-                         const void* packed, void* out, void* stream) {
+}  // extern "C"
+
+// the forward on an explicit path (AUTO resolved here); shared by mglu_forward and
+// mglu_forward_routed
+static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, const void* Wt,
+                                   const void* packed, void* out, void* stream, int path) {
   mglu_status s = check_ptrs(hd, x, B, Wt, packed, out);
   if (s != MGLU_OK) return s;
   hd->last_launches = 0;
   if (B == 0) return MGLU_OK;
-  int path;
-  {
-    std::lock_guard<std::mutex> g(hd->mu);
-    path = hd->path;
-  }
   if (path == MGLU_PATH_AUTO) {
     // measured crossovers at the Llama-3-8B FFN shape (profiles/r01_paths_by_batch.txt): the
     // register-masked HMMA kernel for B <= 4 (one 8-column MMA tile), the stream-K tcgen05 GEMV for
@@ -683,6 +688,69 @@ mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* W
   hd->last_path = path;
   hd->last_launches = launches;
   return MGLU_OK;
+}
+
+extern "C" {
+
+mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* Wt,
+                         const void* packed, void* out, void* stream) {
+  if (!hd) return MGLU_ERR_INVALID_ARG;
+  int path;
+  {
+    std::lock_guard<std::mutex> g(hd->mu);
+    path = hd->path;
+  }
+  return forward_on_path(hd, x, B, Wt, packed, out, stream, path);
+}
+
+mglu_status mglu_router_topk(mglu_handle hd, const void* x, int64_t B, const void* Wr, int K, float* G,
+                             void* stream) {
+  if (!hd) return MGLU_ERR_INVALID_ARG;
+  if (B < 0 || !x || !Wr || !G) return set_err(hd, MGLU_ERR_INVALID_ARG, "null pointer or B < 0");
+  if (K < 1 || K > hd->n_m) return set_err(hd, MGLU_ERR_INVALID_ARG, "K must be in [1, n_m]");
+  if (hd->dtype != MGLU_BF16) return set_err(hd, MGLU_ERR_UNSUPPORTED, "router: bf16 handles only");
+  if (!aligned16(x) || !aligned16(Wr) || !aligned16(G)) return set_err(hd, MGLU_ERR_MISALIGNED, "16-byte alignment");
+  hd->last_launches = 0;
+  if (B == 0) return MGLU_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != hd->device) cudaSetDevice(hd->device);
+  const dim3 grid((unsigned)((B + 7) / 8)), block(256);
+  cudaStream_t st = (cudaStream_t)stream;
+  const auto* xb = (const __nv_bfloat16*)x;
+  const auto* wr = (const __nv_bfloat16*)Wr;
+  cudaError_t e;
+  switch (hd->n_m) {
+    case 1: e = launch_pdl(mglu::router_topk_kernel<1>, grid, block, 0, st, xb, (int)B, (int)hd->d, wr, K, G); break;
+    case 2: e = launch_pdl(mglu::router_topk_kernel<2>, grid, block, 0, st, xb, (int)B, (int)hd->d, wr, K, G); break;
+    case 4: e = launch_pdl(mglu::router_topk_kernel<4>, grid, block, 0, st, xb, (int)B, (int)hd->d, wr, K, G); break;
+    default: e = launch_pdl(mglu::router_topk_kernel<8>, grid, block, 0, st, xb, (int)B, (int)hd->d, wr, K, G); break;
+  }
+  if (prev != hd->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(hd, e, "mglu_router_topk launch");
+  hd->last_launches = 1;
+  return MGLU_OK;
+}
+
+mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* packed,
+                                const float* G, void* out, void* stream) {
+  mglu_status s = check_ptrs(hd, x, B, Wt, packed, out);
+  if (s != MGLU_OK) return s;
+  if (!G) return set_err(hd, MGLU_ERR_INVALID_ARG, "null gate weights");
+  if (!aligned16(G)) return set_err(hd, MGLU_ERR_MISALIGNED, "gate weights must be 16-byte aligned");
+  int path;
+  {
+    std::lock_guard<std::mutex> g(hd->mu);
+    path = hd->path;
+  }
+  if (path == MGLU_PATH_TCGEN05 || path == MGLU_PATH_TCDEC)
+    return set_err(hd, MGLU_ERR_UNSUPPORTED, "routed forward: MMA or SIMT paths only (round 1)");
+  // the routed weights reach the MMA / SIMT launchers through a thread-local pointer
+  if (path == MGLU_PATH_AUTO) path = mma_can_serve(hd, B) ? MGLU_PATH_MMA : MGLU_PATH_SIMT;
+  t_routed_G = G;
+  s = forward_on_path(hd, x, B, Wt, packed, out, stream, path);
+  t_routed_G = nullptr;
+  return s;
 }
 
 mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, const void* Wt,

@@ -61,6 +61,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "mglu_forward": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_forward_partials": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_forward_host": ([vp, vp, i64, vp, vp, vp, vp], c_int),
+        "mglu_router_topk": ([vp, vp, i64, vp, c_int, vp, vp], c_int),
+        "mglu_forward_routed": ([vp, vp, i64, vp, vp, vp, vp, vp], c_int),
         "mglu_packed_mask_bytes": ([i64, i64, c_int], sz),
         "mglu_pack_masks_host": ([vp, c_int, i64, i64, vp], c_int),
         "mglu_pack_logits_host": ([vp, c_int, i64, i64, vp], c_int),
@@ -148,6 +150,16 @@ def mglu_forward_host(handle, x_host, B, Wt, packed, out_host, stream=None) -> N
     _check(load_library().mglu_forward_host(handle, _ptr(x_host), B, _ptr(Wt), _ptr(packed),
                                             _ptr(out_host), _stream_ptr(stream, Wt.device)),
            handle, "mglu_forward_host")
+
+
+def mglu_router_topk(handle, x, B, Wr, K, G, stream=None) -> None:
+    _check(load_library().mglu_router_topk(handle, _ptr(x), B, _ptr(Wr), K, _ptr(G),
+                                           _stream_ptr(stream, x.device)), handle, "mglu_router_topk")
+
+
+def mglu_forward_routed(handle, x, B, Wt, packed, G, out, stream=None) -> None:
+    _check(load_library().mglu_forward_routed(handle, _ptr(x), B, _ptr(Wt), _ptr(packed), _ptr(G), _ptr(out),
+                                              _stream_ptr(stream, x.device)), handle, "mglu_forward_routed")
 
 
 def mglu_packed_mask_bytes(d: int, h: int, n_m: int) -> int:
@@ -255,6 +267,27 @@ class Mglu:
             if st != MGLU_OK:
                 _check(st, self.handle, "mglu_forward")
         return call
+
+    def router_topk(self, x: torch.Tensor, Wr: torch.Tensor, K: int, stream=None) -> torch.Tensor:
+        """G = Softmax(TopK(x W_r)) [B][n_m] fp32 (Appendix B); Wr is [n_m][d] bf16."""
+        if Wr.dtype != torch.bfloat16 or tuple(Wr.shape) != (self.n_m, self.d) or not Wr.is_contiguous():
+            raise MgluError(MGLU_ERR_INVALID_ARG, "Wr must be a contiguous bf16 [n_m][d] tensor")
+        B = x.shape[0]
+        G = torch.empty((B, self.n_m), dtype=torch.float32, device=x.device)
+        mglu_router_topk(self.handle, x.contiguous(), B, Wr, K, G, stream)
+        return G
+
+    def forward_routed(self, x: torch.Tensor, Wt: torch.Tensor, packed: torch.Tensor, G: torch.Tensor,
+                       out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """y = sum_i G[:, i] g(s_i) (t - s_i) (Top-K routed MGLU)."""
+        self._check_inputs(x, Wt, packed)
+        B = x.shape[0]
+        if G.dtype != torch.float32 or tuple(G.shape) != (B, self.n_m) or not G.is_contiguous():
+            raise MgluError(MGLU_ERR_INVALID_ARG, "G must be a contiguous fp32 [B][n_m] tensor")
+        if out is None:
+            out = torch.empty((B, self.h), dtype=TORCH_DTYPE[self.dtype], device=x.device)
+        mglu_forward_routed(self.handle, x, B, Wt, packed, G, out, stream)
+        return out
 
     def forward_partials(self, x, Wt, packed, stream=None) -> torch.Tensor:
         self._check_inputs(x, Wt, packed)

@@ -1,0 +1,119 @@
+"""GPU parity of the Top-K routed MGLU (Appendix B) through the C
+ABI: the router (mglu_router_topk: fp32 logits, TopK with ties to the lowest index, softmax over the
+kept logits) against the oracle's topk_gate, and the routed forward (mglu_forward_routed) against
+the oracle's routed sum built from its independent per-mask gate/value streams -- on the MMA path
+(which skips masks no token selected) and the SIMT path."""
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import TIGHT, TOL, make_inputs, normwise_err, oracle, oracle_inputs, to_device
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_23225_b200.build import build
+    build()
+
+
+def _router_weights(seed, n_m, d):
+    g = torch.Generator().manual_seed(seed)
+    return (torch.randn(n_m, d, generator=g) / d ** 0.5).to(torch.bfloat16)
+
+
+def _oracle_routed(inp, n_m, act_code, G):
+    from oracle import mglu_routed_from_partials
+    xo, Wo = oracle_inputs(inp, "bf16")
+    o = oracle()
+    h = Wo.shape[0]
+    _, z, _ = o.forward(xo, Wo, np.arange(h), o.pack(inp["bits"]), n_m, act_code, want_partials=True)
+    gate = np.transpose(z[:, :n_m, :], (1, 0, 2))
+    value = np.transpose(z[:, n_m:, :], (1, 0, 2))
+    return mglu_routed_from_partials(gate, value, G, act_code)
+
+
+@pytest.mark.parametrize("n_m,K", [(4, 1), (4, 2), (8, 2), (8, 4), (8, 8)])
+@pytest.mark.parametrize("B", [1, 3, 8])
+def test_router_matches_oracle(n_m, K, B):
+    from oracle import router_logits, topk_gate
+    from paper_2506_23225_b200.mglu import Mglu
+    d = 1024
+    inp = make_inputs(300 + n_m + K + B, B=B, d=d, h=128, n_m=n_m, dtype="bf16")
+    x, _ = to_device(inp, "bf16")
+    Wr = _router_weights(7 + n_m, n_m, d)
+    layer = Mglu(d, 128, n_m, dtype="bf16")
+    G = layer.router_topk(x, Wr.cuda(), K).cpu().numpy()
+    xo, _ = oracle_inputs(inp, "bf16")
+    l = router_logits(xo, Wr.float().numpy().astype(np.float64))
+    G_ref = topk_gate(l, K)
+    srt = np.sort(l, axis=1)[:, ::-1]
+    for b in range(B):
+        # the selection is a discrete decision taken in fp32 on the GPU: compare it where the
+        # K-th and (K+1)-th logits are separated by more than the fp32 rounding of a d-term sum
+        if K < n_m and srt[b, K - 1] - srt[b, K] < 1e-4:
+            continue
+        np.testing.assert_array_equal(G[b] != 0, G_ref[b] != 0)
+        np.testing.assert_allclose(G[b], G_ref[b], rtol=0, atol=2e-6)
+    assert np.allclose(G.sum(axis=1), 1.0, atol=1e-6)
+
+
+@pytest.mark.parametrize("path", ["mma", "simt"])
+@pytest.mark.parametrize("n_m,K,B", [(4, 1, 1), (4, 2, 3), (8, 2, 1), (8, 3, 5), (8, 8, 8), (2, 1, 2)])
+def test_routed_forward_matches_oracle(path, n_m, K, B):
+    from oracle import topk_gate
+    from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
+    d, h = 2048, 700
+    inp = make_inputs(500 + n_m * 10 + K + B, B=B, d=d, h=h, n_m=n_m, dtype="bf16")
+    x, Wt = to_device(inp, "bf16")
+    packed = torch.from_numpy(mglu_pack_masks_host(inp["bits"])).cuda()
+    rng = np.random.default_rng(K + B)
+    G = topk_gate(rng.standard_normal((B, n_m)), K)
+    layer = Mglu(d, h, n_m, act="swish", dtype="bf16", path=path)
+    y = layer.forward_routed(x, Wt, packed, torch.from_numpy(G.astype(np.float32)).cuda())
+    torch.cuda.synchronize()
+    assert layer.last_path() == path
+    ref = _oracle_routed(inp, n_m, 1, G.astype(np.float32).astype(np.float64))
+    err = normwise_err(y.float().cpu().numpy().astype(np.float64), ref)
+    assert err <= TOL["bf16"] and err <= TIGHT["bf16"], err
+
+
+def test_router_then_routed_forward_chain():
+    """router -> routed forward on one stream (PDL chain), config-3 shape, B = 1, n_m = 8, K = 2;
+    the oracle applies the GPU's gate weights (the discrete TopK decision is checked above)."""
+    from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
+    d, h, n_m, K = 4096, 1024, 8, 2
+    inp = make_inputs(77, B=1, d=d, h=h, n_m=n_m, dtype="bf16")
+    x, Wt = to_device(inp, "bf16")
+    packed = torch.from_numpy(mglu_pack_masks_host(inp["bits"])).cuda()
+    Wr = _router_weights(3, n_m, d).cuda()
+    layer = Mglu(d, h, n_m, act="swish", dtype="bf16")
+    G = layer.router_topk(x, Wr, K)
+    y = layer.forward_routed(x, Wt, packed, G)
+    torch.cuda.synchronize()
+    assert layer.last_path() == "mma" and int((G != 0).sum()) == K
+    ref = _oracle_routed(inp, n_m, 1, G.cpu().numpy().astype(np.float64))
+    assert normwise_err(y.float().cpu().numpy().astype(np.float64), ref) <= TIGHT["bf16"]
+
+
+def test_routed_errors():
+    from paper_2506_23225_b200.mglu import Mglu, MgluError, MGLU_ERR_INVALID_ARG, MGLU_ERR_UNSUPPORTED
+    d, h, n_m = 512, 256, 4
+    layer = Mglu(d, h, n_m, dtype="bf16")
+    x = torch.zeros(1, d, dtype=torch.bfloat16, device="cuda")
+    Wr = torch.zeros(n_m, d, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(MgluError) as e:
+        layer.router_topk(x, Wr, 0)
+    assert e.value.status == MGLU_ERR_INVALID_ARG
+    with pytest.raises(MgluError) as e:
+        layer.router_topk(x, Wr, n_m + 1)
+    assert e.value.status == MGLU_ERR_INVALID_ARG
+    layer.set_path("tcgen05")
+    Wt = torch.zeros(h, d, dtype=torch.bfloat16, device="cuda")
+    packed = torch.zeros(h * d * n_m // 8, dtype=torch.uint8, device="cuda")
+    with pytest.raises(MgluError) as e:
+        layer.forward_routed(x, Wt, packed, torch.zeros(1, n_m, device="cuda"))
+    assert e.value.status == MGLU_ERR_UNSUPPORTED
