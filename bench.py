@@ -321,16 +321,28 @@ def run_mglu(args, ws, rank, local):
     layer = Mglu(d, h_loc, n_m, act=act, dtype="bf16", device=local, path=args.path)
     stream = torch.cuda.Stream()
 
-    calls = [layer.bind(x, Wt, codes, y, stream=stream) for Wt, codes in layers]
+    if args.topk:
+        # Top-K routed MGLU (Appendix B): a step = router (x W_r, TopK, softmax) + routed forward
+        from paper_2506_23225_b200.mglu import mglu_forward_routed, mglu_router_topk
+        gr = torch.Generator(device="cuda").manual_seed(99)
+        Wr = (torch.randn(n_m, d, device="cuda", generator=gr) / d ** 0.5).to(torch.bfloat16)
+        G = torch.empty(B, n_m, device="cuda", dtype=torch.float32)
 
-    def step(k):
-        calls[k % L]()
+        def step(k):
+            Wt, codes = layers[k % L]
+            mglu_router_topk(layer.handle, x, B, Wr, args.topk, G, stream)
+            mglu_forward_routed(layer.handle, x, B, Wt, codes, G, args.topk, y, stream)
+    else:
+        calls = [layer.bind(x, Wt, codes, y, stream=stream) for Wt, codes in layers]
+
+        def step(k):
+            calls[k % L]()
 
     with torch.cuda.stream(stream):
         for k in range(args.warmup):
             step(k)
         stream.synchronize()
-        launches_per_step = layer.last_launch_count()
+        launches_per_step = layer.last_launch_count() + (1 if args.topk else 0)
         path_used = layer.last_path()
         # clock window + timed region, NVML-sampled
         sampler = ClockSampler(local)
@@ -354,7 +366,9 @@ def run_mglu(args, ws, rank, local):
     units_rank = work(d, h_loc, n_m, B)[0]
     bytes_rank = algorithmic_bytes(d, h_loc, n_m, B)
     value = units_layer * args.steps / el_max / scale
-    per_launch_s = el / args.steps / max(1, launches_per_step)
+    # (routed steps: the router is a d x n_m GEMV next to the layer; the step's two launches are
+    # charged together to the layer's bytes)
+    per_launch_s = el / args.steps / (1 if args.topk else max(1, launches_per_step))
     peaks = load_peaks()
     achieved = units_rank / per_launch_s / scale
     if is_prefill(B):
@@ -367,7 +381,7 @@ def run_mglu(args, ws, rank, local):
     # steps alternate over E streams, each with its own handle (own device staging buffers) and its
     # own pinned host buffers, so one step's copies overlap another step's kernel; the timed region
     # spans every stream (start event joined by all, end after all have drained).
-    E = max(1, args.e2e_streams)
+    E = max(1, args.e2e_streams) if not args.topk else 0
     e_layers = [layer] + [Mglu(d, h_loc, n_m, act=act, dtype="bf16", device=local, path=args.path) for _ in range(E - 1)]
     e_streams = [stream] + [torch.cuda.Stream() for _ in range(E - 1)]
     xh = [x.cpu().pin_memory() for _ in range(E)]
@@ -392,18 +406,21 @@ def run_mglu(args, ws, rank, local):
         ev1.synchronize()
         return ev0.elapsed_time(ev1) / 1e3
 
-    for k in range(max(3, args.warmup)):
-        step_host(k)
-    torch.cuda.synchronize()
-    barrier(ws)
-    el_e2e = time_e2e(args.steps)
-    barrier(ws)
-    el_e2e = max_over_ranks(ws, el_e2e)
-    e2e = {"value": units_layer * args.steps / el_e2e / scale, "unit": unit,
-           "h2d_bytes_per_step": B * d * 2 * ws, "d2h_bytes_per_step": B * h * 2,
-           "us_per_call": el_e2e / args.steps * 1e6, "streams": E,
-           "how": "mglu_forward_host per step (pinned x -> device, forward, y -> pinned host), steps alternating over "
-                  f"{E} streams/handles so copies overlap kernels"}
+    if not E:
+        e_layers, e2e = [layer], None
+    else:
+        for k in range(max(3, args.warmup)):
+            step_host(k)
+        torch.cuda.synchronize()
+        barrier(ws)
+        el_e2e = time_e2e(args.steps)
+        barrier(ws)
+        el_e2e = max_over_ranks(ws, el_e2e)
+        e2e = {"value": units_layer * args.steps / el_e2e / scale, "unit": unit,
+               "h2d_bytes_per_step": B * d * 2 * ws, "d2h_bytes_per_step": B * h * 2,
+               "us_per_call": el_e2e / args.steps * 1e6, "streams": E,
+               "how": "mglu_forward_host per step (pinned x -> device, forward, y -> pinned host), steps "
+                      f"alternating over {E} streams/handles so copies overlap kernels"}
     for extra in e_layers[1:]:
         extra.close()
 
@@ -424,7 +441,8 @@ def run_mglu(args, ws, rank, local):
             "config": {"workload": desc, "d": d, "h": h, "n_m": n_m, "batch": B, "act": act,
                        "parallelism": f"column-shard h/{ws}" if ws > 1 else "single GPU",
                        "l2": f"inputs larger than L2: {L} distinct layer copies ({L * bytes_rank / 1e6:.0f} MB/rank) rotated, no flush",
-                       "kernel_path": path_used, "launch": "PDL (programmatic dependent launch) per call"},
+                       "kernel_path": path_used, "launch": "PDL (programmatic dependent launch) per call",
+                       **({"topk": args.topk, "step": "router_topk + forward_routed (2 launches)"} if args.topk else {})},
             "us_per_call": el_max / args.steps * 1e6,
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                          "frac": achieved / peak, "traffic": traffic,
@@ -460,6 +478,7 @@ def main(argv=None):
     ap.add_argument("--clock-window", type=float, default=0.3)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--e2e-streams", type=int, default=2, help="streams the e2e (host-buffer) leg alternates over")
+    ap.add_argument("--topk", type=int, default=0, help="Top-K routed MGLU: K kept masks (router + routed forward)")
     ap.add_argument("--no-comparator", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shape", default=None, help="experiment: d,h,n_m,B (overrides --workload)")

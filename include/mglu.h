@@ -130,14 +130,16 @@ mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, cons
  *   Errors: INVALID_ARG (nulls, B < 0, K out of range), MISALIGNED, UNSUPPORTED (fp32), CUDA.
  * mglu_forward_routed: y[b][j] = sum_i G[b][i] g(s_i) (t - s_i) in one pass over W and
  *   the codes, G [B][n_m] fp32 on the device (e.g. from mglu_router_topk on the same stream; read
- *   after the predecessor completes).  Masks whose weight is 0 for every token of the call are not
- *   evaluated (MMA path: their sign flips and MMAs are skipped).  Runs the MMA path (bf16,
- *   B <= 8) or the SIMT path; forcing TCGEN05/TCDEC returns UNSUPPORTED in this version.
- *   Errors as mglu_forward, plus INVALID_ARG / MISALIGNED for G. */
+ *   after the predecessor completes).  K (0..n_m) promises at most K nonzero weights per token (as
+ *   produced by mglu_router_topk with that K); 0 = no promise.  With K > 0 the MMA path evaluates
+ *   only the masks some token of the call selected (at most min(n_m, B*K); their sign flips and MMAs,
+ *   Swish only -- other activations evaluate every mask); a G violating the promise gives undefined
+ *   output.  Runs the MMA path (bf16, B <= 8) or the SIMT path; forcing TCGEN05/TCDEC returns
+ *   UNSUPPORTED in this version.  Errors as mglu_forward, plus INVALID_ARG (K) / MISALIGNED for G. */
 mglu_status mglu_router_topk(mglu_handle hd, const void* x, int64_t B, const void* Wr, int K, float* G,
                              void* stream);
 mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* packed,
-                                const float* G, void* out, void* stream);
+                                const float* G, int K, void* out, void* stream);
 
 /* End-to-end form: x_host [B][d] and out_host [B][h] are HOST buffers (pinned for async
  * copies; pageable works but serialises).  Copies x to the handle's device staging buffer,

@@ -69,7 +69,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t lin, uint32_t rb) {
   return lin ^ (((lin >> 7) & (rb / 16 - 1)) << 4);
 }
 
-template <int NM, int ACT, int NB>
+template <int NM, int ACT, int NB, int KSEL>
 __global__ void __launch_bounds__(kDecThreads, 1)
 gemv_mma_kernel(const DecParams p,
                 const __grid_constant__ CUtensorMap mW64, const __grid_constant__ CUtensorMap mC64,
@@ -77,7 +77,7 @@ gemv_mma_kernel(const DecParams p,
                 const __grid_constant__ CUtensorMap mWb, const __grid_constant__ CUtensorMap mCb) {
   constexpr int SPAN = dec_code_span<NM>();
   constexpr int SB = dec_stage_bytes<NM>();
-  constexpr int NACC = NB * (NM + 1);
+  constexpr int NACC = NB * ((KSEL > 0 ? KSEL : NM) + 1);
   extern __shared__ __align__(1024) uint8_t smem[];
   const int S = p.stages;
   uint8_t* ring = smem;
@@ -161,20 +161,33 @@ gemv_mma_kernel(const DecParams p,
       xs[(size_t)(2 * b + (q & 1)) * p.xpar + (q >> 1)] = val;
     }
   }
-  // routed forward: masks with zero weight for every token of the batch are skipped entirely
-  // (their HMMAs and sign flips; uniform across the CTA)
-  uint32_t active = (1u << NM) - 1u;
-  if (p.G) {
-    active = 0u;
+  // KSEL > 0: Top-K routed forward (Appendix B).  Only the masks some token of the batch selected
+  // (nonzero G) are evaluated: up to KSEL of them, gathered into slots sel[0..KSEL) (uniform
+  // across the CTA); unused slots repeat slot 0 with valid = false (computed, weighted 0).
+  constexpr int NSLOT = KSEL > 0 ? KSEL : NM;              // masked accumulators
+  int sel[NSLOT];
+  uint32_t valid = (1u << NSLOT) - 1u;
+#pragma unroll
+  for (int k = 0; k < NSLOT; ++k) sel[k] = k;
+  if constexpr (KSEL > 0) {
+    uint32_t active = 0u;
     for (int q = 0; q < B * NM; ++q) active |= (p.G[q] != 0.0f ? 1u : 0u) << (q % NM);
+    valid = 0u;
+    int n = 0;
+#pragma unroll
+    for (int i = 0; i < NM; ++i)
+      if (((active >> i) & 1u) && n < KSEL) { sel[n] = i; valid |= 1u << n; ++n; }
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k)
+      if (!((valid >> k) & 1u)) sel[k] = sel[0];
   }
   named_bar_sync(1, kDecConsumers * 32);
 
-  float acc[NB][NM + 1][4];
+  float acc[NB][NSLOT + 1][4];
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-    for (int a = 0; a <= NM; ++a)
+    for (int a = 0; a <= NSLOT; ++a)
 #pragma unroll
       for (int v = 0; v < 4; ++v) acc[nb][a][v] = 0.f;
 
@@ -200,6 +213,15 @@ gemv_mma_kernel(const DecParams p,
       // the step's 32-column group (group st of code block kp): n_m words (16-byte chunks swizzled)
       coff[st] = (uint32_t)kDecWBytes + swz((uint32_t)((kp * rows + srow) * SPAN + st * 4 * NM), SPAN);
     }
+    // routed: the selected masks' words (one 4-byte read per slot and step)
+    uint32_t csel[KSEL > 0 ? KSEL : 1][4];
+    if constexpr (KSEL > 0) {
+#pragma unroll
+      for (int k = 0; k < KSEL; ++k)
+#pragma unroll
+        for (int st = 0; st < 4; ++st)
+          csel[k][st] = (uint32_t)kDecWBytes + swz((uint32_t)((kp * rows + srow) * SPAN + (st * NM + sel[k]) * 4), SPAN);
+    }
     // x: word index of pair 4c of step 0 of stage 0 for this lane's token column (token B = zeros)
     uint32_t xoff[NB];
 #pragma unroll
@@ -216,7 +238,11 @@ gemv_mma_kernel(const DecParams p,
 #pragma unroll
         for (int st = 0; st < 4; ++st) {
           const uint4 wq = *reinterpret_cast<const uint4*>(wst + woff[st]);
-          uint32_t mw[NM];
+          uint32_t mw[NSLOT];
+          if constexpr (KSEL > 0) {
+#pragma unroll
+            for (int k = 0; k < KSEL; ++k) mw[k] = *reinterpret_cast<const uint32_t*>(wst + csel[k][st]);
+          } else
 #pragma unroll
           for (int q = 0; q < (NM + 3) / 4; ++q) {
             // n_m = 8: the second 16-byte chunk is the next one in the swizzled span
@@ -240,8 +266,7 @@ gemv_mma_kernel(const DecParams p,
           for (int nb = 0; nb < NB; ++nb) mma_16816(acc[nb][0], wq.x, wq.y, wq.z, wq.w, xb[nb][0], xb[nb][1]);
           // u_i += x (sigma_i (.) W): pair q of the thread's 8 columns is register q of the quad
 #pragma unroll
-          for (int ii = 0; ii < NM; ++ii) {
-            if (!((active >> ii) & 1u)) continue;
+          for (int ii = 0; ii < NSLOT; ++ii) {
             const uint32_t a0 = sign_flip(wq.x, mw[ii], mul[0]), a1 = sign_flip(wq.y, mw[ii], mul[1]);
             const uint32_t a2 = sign_flip(wq.z, mw[ii], mul[2]), a3 = sign_flip(wq.w, mw[ii], mul[3]);
 #pragma unroll
@@ -257,11 +282,11 @@ gemv_mma_kernel(const DecParams p,
     // a5: (even pairs, even column) + (odd pairs, odd column) -> one value per (row, token)
     // and accumulator; parts kp >= 1 hand theirs to part 0 through smem (fixed order).  The round
     // ends at the same stage for every warp, so one consumer-wide barrier pair serves all tiles.
-    float v[NB][NM + 1];
+    float v[NB][NSLOT + 1];
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-      for (int a = 0; a <= NM; ++a) {
+      for (int a = 0; a <= NSLOT; ++a) {
         v[nb][a] = acc[nb][a][0] + acc[nb][a][3];
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[nb][a][q] = 0.f;
@@ -271,7 +296,7 @@ gemv_mma_kernel(const DecParams p,
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-        for (int a = 0; a <= NM; ++a) pw[nb * (NM + 1) + a] = v[nb][a];
+        for (int a = 0; a <= NSLOT; ++a) pw[nb * (NSLOT + 1) + a] = v[nb][a];
     }
     named_bar_sync(1, kDecConsumers * 32);                  // the producer keeps streaming meanwhile
     if (live && kp == 0) {
@@ -280,17 +305,26 @@ gemv_mma_kernel(const DecParams p,
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-          for (int a = 0; a <= NM; ++a) v[nb][a] += pq[nb * (NM + 1) + a];
+          for (int a = 0; a <= NSLOT; ++a) v[nb][a] += pq[nb * (NSLOT + 1) + a];
       }
       const int row = rho * kDecFullRows + tl * 8 + prow;
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) {
         const int tok = nb * 4 + c;
         if (tok < B && row < nrows) {
-          float sv[NM];
+          float sv[NSLOT];
 #pragma unroll
-          for (int ii = 0; ii < NM; ++ii) sv[ii] = 0.5f * (v[nb][0] + v[nb][1 + ii]);   // s_i = (t + u_i) / 2
-          const float y = mglu_epilogue_w<ACT, NM>(v[nb][0], sv, p.G ? p.G + (size_t)tok * NM : nullptr);   // Eq. 3 / routed
+          for (int ii = 0; ii < NSLOT; ++ii) sv[ii] = 0.5f * (v[nb][0] + v[nb][1 + ii]);   // s_i = (t + u_i) / 2
+          float y;
+          if constexpr (KSEL > 0) {                         // routed: slot k is mask sel[k], weight G
+            y = 0.f;
+            const float* gw = p.G + (size_t)tok * NM;
+#pragma unroll
+            for (int k = 0; k < KSEL; ++k)
+              if ((valid >> k) & 1u) y = fmaf(gw[sel[k]] * act_g<ACT>(sv[k]), v[nb][0] - sv[k], y);
+          } else {
+            y = mglu_epilogue_w<ACT, NM>(v[nb][0], sv, p.G ? p.G + (size_t)tok * NM : nullptr);   // Eq. 3 (or all-mask routed)
+          }
           p.out[(size_t)tok * p.h + r0 + row] = __float2bfloat16_rn(y);
         }
       }

@@ -61,6 +61,7 @@ namespace {
 // gate weights of the routed forward being enqueued by this host thread (nullptr: plain forward);
 // set and cleared by mglu_forward_routed around the regular dispatch
 thread_local const float* t_routed_G = nullptr;
+thread_local int t_routed_K = 0;   // K of the routed call (0: unknown -> every mask evaluated)
 
 const char* kStatusStr[] = {"MGLU_OK", "MGLU_ERR_INVALID_ARG", "MGLU_ERR_UNSUPPORTED",
                             "MGLU_ERR_MISALIGNED", "MGLU_ERR_CUDA", "MGLU_ERR_OOM"};
@@ -220,7 +221,7 @@ bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, int rem_a, int re
   return true;
 }
 
-template <int NM, int ACT, int NB>
+template <int NM, int ACT, int NB, int KSEL>
 cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
                        void* out, cudaStream_t st) {
   mglu::DecParams p;
@@ -249,7 +250,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   p.xpar = npair / 2 + 8;
   constexpr size_t SB = mglu::dec_stage_bytes<NM>();
   const size_t xbytes = (size_t)2 * (B + 1) * p.xpar * 4;   // + an all-zero token row
-  const size_t partbytes = (size_t)mglu::kDecConsumers * 32 * NB * (NM + 1) * 4;
+  const size_t partbytes = (size_t)mglu::kDecConsumers * 32 * NB * ((KSEL > 0 ? KSEL : NM) + 1) * 4;
   const size_t fixed = xbytes + partbytes + 1024;
   const size_t cap = std::min<size_t>((size_t)hd->max_smem_optin, 200 * 1024);
   if (cap < fixed) return cudaErrorInvalidConfiguration;
@@ -258,7 +259,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   if (S < 2) return cudaErrorInvalidConfiguration;
   p.stages = S;
   const size_t smem = (size_t)S * SB + 2 * S * sizeof(uint64_t) + partbytes + xbytes;
-  auto kern = mglu::gemv_mma_kernel<NM, ACT, NB>;
+  auto kern = mglu::gemv_mma_kernel<NM, ACT, NB, KSEL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(kern, dim3((unsigned)ncta), dim3(mglu::kDecThreads), smem, st, p, maps[0], maps[1], maps[2],
@@ -268,8 +269,23 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
 template <int NM, int ACT>
 cudaError_t run_mma(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
                     void* out, cudaStream_t st) {
-  return B <= 4 ? run_mma_nb<NM, ACT, 1>(hd, x, B, Wt, codes, out, st)
-                : run_mma_nb<NM, ACT, 2>(hd, x, B, Wt, codes, out, st);
+  // routed (Top-K) swish forward: evaluate only the masks some token selected -- at most K per
+  // token, so min(n_m, B*K) slots, rounded up to a power of two (other activations and larger
+  // unions run all masks with the weights in the epilogue)
+  if constexpr (ACT == mglu::kSwish && NM >= 2) {
+    if (t_routed_G && t_routed_K > 0) {
+      const int u = std::min(NM, B * t_routed_K);
+      if (u <= 1) return B <= 4 ? run_mma_nb<NM, ACT, 1, 1>(hd, x, B, Wt, codes, out, st)
+                                : run_mma_nb<NM, ACT, 2, 1>(hd, x, B, Wt, codes, out, st);
+      if (u <= 2 && NM > 2) return B <= 4 ? run_mma_nb<NM, ACT, 1, 2>(hd, x, B, Wt, codes, out, st)
+                                          : run_mma_nb<NM, ACT, 2, 2>(hd, x, B, Wt, codes, out, st);
+      if constexpr (NM == 8)
+        if (u <= 4) return B <= 4 ? run_mma_nb<NM, ACT, 1, 4>(hd, x, B, Wt, codes, out, st)
+                                  : run_mma_nb<NM, ACT, 2, 4>(hd, x, B, Wt, codes, out, st);
+    }
+  }
+  return B <= 4 ? run_mma_nb<NM, ACT, 1, 0>(hd, x, B, Wt, codes, out, st)
+                : run_mma_nb<NM, ACT, 2, 0>(hd, x, B, Wt, codes, out, st);
 }
 
 template <int NM>
@@ -715,7 +731,7 @@ mglu_status mglu_router_topk(mglu_handle hd, const void* x, int64_t B, const voi
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != hd->device) cudaSetDevice(hd->device);
-  const dim3 grid((unsigned)((B + 7) / 8)), block(256);
+  const dim3 grid((unsigned)B), block(256);              // one CTA per token
   cudaStream_t st = (cudaStream_t)stream;
   const auto* xb = (const __nv_bfloat16*)x;
   const auto* wr = (const __nv_bfloat16*)Wr;
@@ -733,10 +749,11 @@ mglu_status mglu_router_topk(mglu_handle hd, const void* x, int64_t B, const voi
 }
 
 mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* packed,
-                                const float* G, void* out, void* stream) {
+                                const float* G, int K, void* out, void* stream) {
   mglu_status s = check_ptrs(hd, x, B, Wt, packed, out);
   if (s != MGLU_OK) return s;
   if (!G) return set_err(hd, MGLU_ERR_INVALID_ARG, "null gate weights");
+  if (K < 0 || K > hd->n_m) return set_err(hd, MGLU_ERR_INVALID_ARG, "K must be in [0, n_m]");
   if (!aligned16(G)) return set_err(hd, MGLU_ERR_MISALIGNED, "gate weights must be 16-byte aligned");
   int path;
   {
@@ -748,8 +765,10 @@ mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const 
   // the routed weights reach the MMA / SIMT launchers through a thread-local pointer
   if (path == MGLU_PATH_AUTO) path = mma_can_serve(hd, B) ? MGLU_PATH_MMA : MGLU_PATH_SIMT;
   t_routed_G = G;
+  t_routed_K = K;
   s = forward_on_path(hd, x, B, Wt, packed, out, stream, path);
   t_routed_G = nullptr;
+  t_routed_K = 0;
   return s;
 }
 

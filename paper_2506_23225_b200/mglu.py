@@ -62,7 +62,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "mglu_forward_partials": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_forward_host": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_router_topk": ([vp, vp, i64, vp, c_int, vp, vp], c_int),
-        "mglu_forward_routed": ([vp, vp, i64, vp, vp, vp, vp, vp], c_int),
+        "mglu_forward_routed": ([vp, vp, i64, vp, vp, vp, c_int, vp, vp], c_int),
         "mglu_packed_mask_bytes": ([i64, i64, c_int], sz),
         "mglu_pack_masks_host": ([vp, c_int, i64, i64, vp], c_int),
         "mglu_pack_logits_host": ([vp, c_int, i64, i64, vp], c_int),
@@ -157,8 +157,8 @@ def mglu_router_topk(handle, x, B, Wr, K, G, stream=None) -> None:
                                            _stream_ptr(stream, x.device)), handle, "mglu_router_topk")
 
 
-def mglu_forward_routed(handle, x, B, Wt, packed, G, out, stream=None) -> None:
-    _check(load_library().mglu_forward_routed(handle, _ptr(x), B, _ptr(Wt), _ptr(packed), _ptr(G), _ptr(out),
+def mglu_forward_routed(handle, x, B, Wt, packed, G, K, out, stream=None) -> None:
+    _check(load_library().mglu_forward_routed(handle, _ptr(x), B, _ptr(Wt), _ptr(packed), _ptr(G), K, _ptr(out),
                                               _stream_ptr(stream, x.device)), handle, "mglu_forward_routed")
 
 
@@ -278,7 +278,7 @@ class Mglu:
         return G
 
     def forward_routed(self, x: torch.Tensor, Wt: torch.Tensor, packed: torch.Tensor, G: torch.Tensor,
-                       out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+                       K: int = 0, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """y = sum_i G[:, i] g(s_i) (t - s_i) (Top-K routed MGLU)."""
         self._check_inputs(x, Wt, packed)
         B = x.shape[0]
@@ -286,7 +286,7 @@ class Mglu:
             raise MgluError(MGLU_ERR_INVALID_ARG, "G must be a contiguous fp32 [B][n_m] tensor")
         if out is None:
             out = torch.empty((B, self.h), dtype=TORCH_DTYPE[self.dtype], device=x.device)
-        mglu_forward_routed(self.handle, x, B, Wt, packed, G, out, stream)
+        mglu_forward_routed(self.handle, x, B, Wt, packed, G, K, out, stream)
         return out
 
     def forward_partials(self, x, Wt, packed, stream=None) -> torch.Tensor:

@@ -62,7 +62,8 @@ def test_router_matches_oracle(n_m, K, B):
 
 
 @pytest.mark.parametrize("path", ["mma", "simt"])
-@pytest.mark.parametrize("n_m,K,B", [(4, 1, 1), (4, 2, 3), (8, 2, 1), (8, 3, 5), (8, 8, 8), (2, 1, 2)])
+@pytest.mark.parametrize("n_m,K,B", [(4, 1, 1), (4, 2, 3), (8, 2, 1), (8, 3, 5), (8, 8, 8), (2, 1, 2), (8, 1, 2),
+                                     (8, 4, 1), (8, 2, 2)])
 def test_routed_forward_matches_oracle(path, n_m, K, B):
     from oracle import topk_gate
     from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
@@ -73,12 +74,29 @@ def test_routed_forward_matches_oracle(path, n_m, K, B):
     rng = np.random.default_rng(K + B)
     G = topk_gate(rng.standard_normal((B, n_m)), K)
     layer = Mglu(d, h, n_m, act="swish", dtype="bf16", path=path)
-    y = layer.forward_routed(x, Wt, packed, torch.from_numpy(G.astype(np.float32)).cuda())
+    y = layer.forward_routed(x, Wt, packed, torch.from_numpy(G.astype(np.float32)).cuda(), K)
     torch.cuda.synchronize()
     assert layer.last_path() == path
     ref = _oracle_routed(inp, n_m, 1, G.astype(np.float32).astype(np.float64))
     err = normwise_err(y.float().cpu().numpy().astype(np.float64), ref)
     assert err <= TOL["bf16"] and err <= TIGHT["bf16"], err
+
+
+def test_routed_forward_no_promise_and_other_activation():
+    """K = 0 (no sparsity promise: every mask evaluated) and a non-Swish activation (weights in the
+    epilogue only) give the same routed sum as the oracle."""
+    from oracle import topk_gate
+    from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
+    d, h, n_m, B = 1024, 300, 8, 2
+    inp = make_inputs(901, B=B, d=d, h=h, n_m=n_m, dtype="bf16")
+    x, Wt = to_device(inp, "bf16")
+    packed = torch.from_numpy(mglu_pack_masks_host(inp["bits"])).cuda()
+    G = topk_gate(np.random.default_rng(5).standard_normal((B, n_m)), 2).astype(np.float32)
+    for act, code, K in (("swish", 1, 0), ("gelu", 2, 2), ("sigmoid", 4, 2)):
+        layer = Mglu(d, h, n_m, act=act, dtype="bf16", path="mma")
+        y = layer.forward_routed(x, Wt, packed, torch.from_numpy(G).cuda(), K)
+        ref = _oracle_routed(inp, n_m, code, G.astype(np.float64))
+        assert normwise_err(y.float().cpu().numpy().astype(np.float64), ref) <= TIGHT["bf16"], act
 
 
 def test_router_then_routed_forward_chain():
@@ -92,7 +110,7 @@ def test_router_then_routed_forward_chain():
     Wr = _router_weights(3, n_m, d).cuda()
     layer = Mglu(d, h, n_m, act="swish", dtype="bf16")
     G = layer.router_topk(x, Wr, K)
-    y = layer.forward_routed(x, Wt, packed, G)
+    y = layer.forward_routed(x, Wt, packed, G, K)
     torch.cuda.synchronize()
     assert layer.last_path() == "mma" and int((G != 0).sum()) == K
     ref = _oracle_routed(inp, n_m, 1, G.cpu().numpy().astype(np.float64))
@@ -115,5 +133,5 @@ def test_routed_errors():
     Wt = torch.zeros(h, d, dtype=torch.bfloat16, device="cuda")
     packed = torch.zeros(h * d * n_m // 8, dtype=torch.uint8, device="cuda")
     with pytest.raises(MgluError) as e:
-        layer.forward_routed(x, Wt, packed, torch.zeros(1, n_m, device="cuda"))
+        layer.forward_routed(x, Wt, packed, torch.zeros(1, n_m, device="cuda"), 1)
     assert e.value.status == MGLU_ERR_UNSUPPORTED
