@@ -321,7 +321,25 @@ def run_mglu(args, ws, rank, local):
     layer = Mglu(d, h_loc, n_m, act=act, dtype="bf16", device=local, path=args.path)
     stream = torch.cuda.Stream()
 
-    if args.topk:
+    if args.ffn:
+        # SwiMGLU FFN block (row f1): column-sharded up-projection, row-sharded dense W_o (an
+        # n_m = 0 handle) and, across ranks, one fp32 all-reduce of the [B][d] partials
+        down = Mglu(h_loc, d, 0, act="identity", dtype="bf16", device=local)
+        gw = torch.Generator(device="cuda").manual_seed(7 + rank)
+        Wos = [((torch.rand(d, h_loc, device="cuda", generator=gw) * 2 - 1) / h ** 0.5).to(torch.bfloat16)
+               for _ in range(L)]
+        yd = torch.empty(B, d, device="cuda", dtype=torch.bfloat16)
+        up_calls = [layer.bind(x, Wt, codes, y, stream=stream) for Wt, codes in layers]
+        down_calls = [down.bind(y, Wo, None, yd, stream=stream) for Wo in Wos]
+
+        def step(k):
+            up_calls[k % L]()
+            down_calls[k % L]()
+            if ws > 1:
+                import torch.distributed as dist
+                part = yd.float()
+                dist.all_reduce(part)
+    elif args.topk:
         # Top-K routed MGLU (Appendix B): a step = router (x W_r, TopK, softmax) + routed forward
         from paper_2506_23225_b200.mglu import mglu_forward_routed, mglu_router_topk
         gr = torch.Generator(device="cuda").manual_seed(99)
@@ -342,7 +360,7 @@ def run_mglu(args, ws, rank, local):
         for k in range(args.warmup):
             step(k)
         stream.synchronize()
-        launches_per_step = layer.last_launch_count() + (1 if args.topk else 0)
+        launches_per_step = layer.last_launch_count() + (1 if (args.topk or args.ffn) else 0)
         path_used = layer.last_path()
         # clock window + timed region, NVML-sampled
         sampler = ClockSampler(local)
@@ -365,10 +383,15 @@ def run_mglu(args, ws, rank, local):
     units_layer, scale, unit, metric = work(d, h, n_m, B)
     units_rank = work(d, h_loc, n_m, B)[0]
     bytes_rank = algorithmic_bytes(d, h_loc, n_m, B)
+    if args.ffn:                                              # + the dense W_o pass (x = y, out = [B][d])
+        units_layer += algorithmic_bytes(h, d, 0, B)
+        units_rank += algorithmic_bytes(h_loc, d, 0, B)
+        bytes_rank += algorithmic_bytes(h_loc, d, 0, B)
+        metric = "SwiMGLU FFN block (up-proj + W_o) HBM GB/s at batch B (algorithmic bytes of both layers / time per step)"
     value = units_layer * args.steps / el_max / scale
     # (routed steps: the router is a d x n_m GEMV next to the layer; the step's two launches are
     # charged together to the layer's bytes)
-    per_launch_s = el / args.steps / (1 if args.topk else max(1, launches_per_step))
+    per_launch_s = el / args.steps / (1 if (args.topk or args.ffn) else max(1, launches_per_step))
     peaks = load_peaks()
     achieved = units_rank / per_launch_s / scale
     if is_prefill(B):
@@ -381,7 +404,7 @@ def run_mglu(args, ws, rank, local):
     # steps alternate over E streams, each with its own handle (own device staging buffers) and its
     # own pinned host buffers, so one step's copies overlap another step's kernel; the timed region
     # spans every stream (start event joined by all, end after all have drained).
-    E = max(1, args.e2e_streams) if not args.topk else 0
+    E = max(1, args.e2e_streams) if not (args.topk or args.ffn) else 0
     e_layers = [layer] + [Mglu(d, h_loc, n_m, act=act, dtype="bf16", device=local, path=args.path) for _ in range(E - 1)]
     e_streams = [stream] + [torch.cuda.Stream() for _ in range(E - 1)]
     xh = [x.cpu().pin_memory() for _ in range(E)]
@@ -442,7 +465,8 @@ def run_mglu(args, ws, rank, local):
                        "parallelism": f"column-shard h/{ws}" if ws > 1 else "single GPU",
                        "l2": f"inputs larger than L2: {L} distinct layer copies ({L * bytes_rank / 1e6:.0f} MB/rank) rotated, no flush",
                        "kernel_path": path_used, "launch": "PDL (programmatic dependent launch) per call",
-                       **({"topk": args.topk, "step": "router_topk + forward_routed (2 launches)"} if args.topk else {})},
+                       **({"topk": args.topk, "step": "router_topk + forward_routed (2 launches)"} if args.topk else {}),
+                       **({"ffn": True, "step": "MGLU up-proj + dense W_o (+ fp32 all-reduce across ranks)"} if args.ffn else {})},
             "us_per_call": el_max / args.steps * 1e6,
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                          "frac": achieved / peak, "traffic": traffic,
@@ -479,6 +503,7 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--e2e-streams", type=int, default=2, help="streams the e2e (host-buffer) leg alternates over")
     ap.add_argument("--topk", type=int, default=0, help="Top-K routed MGLU: K kept masks (router + routed forward)")
+    ap.add_argument("--ffn", action="store_true", help="FFN block: up-projection + dense W_o (+ all-reduce under torchrun)")
     ap.add_argument("--no-comparator", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shape", default=None, help="experiment: d,h,n_m,B (overrides --workload)")

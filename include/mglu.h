@@ -98,7 +98,10 @@ typedef enum {
 
 /* Create a handle for one (d, h, n_m, act, dtype) layer on CUDA device `device`.
  *   d, h >= 1; d % 32 == 0 (the 32-column groups of the packed layout, reading R3);
- *   n_m in {1, 2, 4, 8}.
+ *   n_m in {1, 2, 4, 8}, or n_m = 0 for a DENSE projection out = x Wt^T (no masks, no activation;
+ *   `packed` may be NULL) -- the FFN down-projection W_o of SURVEY row f1 (bf16, MMA path,
+ *   1 <= B <= 8, d % 128 == 0, x staged in shared memory: about 4 (B + 1) d bytes must fit next to
+ *   two 32 KB stages; other configurations return UNSUPPORTED or CUDA from mglu_forward).
  * Errors: INVALID_ARG (null out, bad enum, d/h < 1), UNSUPPORTED (n_m, d % 32), CUDA, OOM. */
 mglu_status mglu_create(mglu_handle* out, int64_t d, int64_t h, int n_m, int act, int dtype,
                         int device);

@@ -46,7 +46,7 @@ constexpr int kDecFullRows = 8 * kDecFullTiles;        // 64
 constexpr int kDecWBytes = kDecConsumers * 2048;       // W region of a stage slot (max over rounds)
 
 // mask bytes of one 128-column block of a row: 4 groups x n_m words (TMA box inner span = swizzle span)
-template <int NM> __host__ __device__ constexpr int dec_code_span() { return 16 * NM; }
+template <int NM> __host__ __device__ constexpr int dec_code_span() { return 16 * NM; }   // 0: dense (n_m = 0)
 // stage slot = W region + codes region (rows x WPT blocks x 16 NM bytes <= 128 * consumers * NM)
 template <int NM> __host__ __device__ constexpr int dec_stage_bytes() { return kDecWBytes + 128 * kDecConsumers * NM; }
 
@@ -116,8 +116,9 @@ gemv_mma_kernel(const DecParams p,
       // no over-read of the neighbouring CTA's rows (one descriptor pair per CTA row count)
       const CUtensorMap* mWr = rem == p.rem_a ? &mWa : &mWb;
       const CUtensorMap* mCr = rem == p.rem_a ? &mCa : &mCb;
-      prefetch_tmap(&mW64); prefetch_tmap(&mC64);
-      if (rem) { prefetch_tmap(mWr); prefetch_tmap(mCr); }
+      prefetch_tmap(&mW64);
+      if (NM > 0) prefetch_tmap(&mC64);
+      if (rem) { prefetch_tmap(mWr); if (NM > 0) prefetch_tmap(mCr); }
       const uint64_t pol = policy_evict_first();
       int s = 0;
       uint32_t ph = 0;
@@ -132,7 +133,8 @@ gemv_mma_kernel(const DecParams p,
         uint8_t* wst = ring + (size_t)s * SB;
         mbar_arrive_expect_tx(&full[s], (uint32_t)(rows * wpt * (2 * 128 + SPAN)));
         tma_load_3d_hint(wst, is_full ? &mW64 : mWr, 0, r0 + rho * kDecFullRows, k0 / 64, &full[s], pol);
-        tma_load_3d_hint(wst + kDecWBytes, is_full ? &mC64 : mCr, 0, r0 + rho * kDecFullRows, k0 / 128, &full[s], pol);
+        if constexpr (NM > 0)
+          tma_load_3d_hint(wst + kDecWBytes, is_full ? &mC64 : mCr, 0, r0 + rho * kDecFullRows, k0 / 128, &full[s], pol);
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
@@ -165,7 +167,7 @@ gemv_mma_kernel(const DecParams p,
   // (nonzero G) are evaluated: up to KSEL of them, gathered into slots sel[0..KSEL) (uniform
   // across the CTA); unused slots repeat slot 0 with valid = false (computed, weighted 0).
   constexpr int NSLOT = KSEL > 0 ? KSEL : NM;              // masked accumulators
-  int sel[NSLOT];
+  int sel[NSLOT > 0 ? NSLOT : 1];
   uint32_t valid = (1u << NSLOT) - 1u;
 #pragma unroll
   for (int k = 0; k < NSLOT; ++k) sel[k] = k;
@@ -183,7 +185,7 @@ gemv_mma_kernel(const DecParams p,
   }
   named_bar_sync(1, kDecConsumers * 32);
 
-  float acc[NB][NSLOT + 1][4];
+  float acc[NB][NSLOT + 1][4];   // [0] = t; NM = 0 (dense projection): t only
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
@@ -211,7 +213,8 @@ gemv_mma_kernel(const DecParams p,
       // A: pairs 4c..4c+3 of step st = one swizzled 16-byte read of W block (2 kp + st/2)
       woff[st] = swz((uint32_t)(((2 * kp + (st >> 1)) * rows + srow) * 128 + (32 * (st & 1) + 8 * c) * 2), 128);
       // the step's 32-column group (group st of code block kp): n_m words (16-byte chunks swizzled)
-      coff[st] = (uint32_t)kDecWBytes + swz((uint32_t)((kp * rows + srow) * SPAN + st * 4 * NM), SPAN);
+      if constexpr (NM > 0) coff[st] = (uint32_t)kDecWBytes + swz((uint32_t)((kp * rows + srow) * SPAN + st * 4 * NM), SPAN);
+      else coff[st] = 0u;
     }
     // routed: the selected masks' words (one 4-byte read per slot and step)
     uint32_t csel[KSEL > 0 ? KSEL : 1][4];
@@ -238,11 +241,11 @@ gemv_mma_kernel(const DecParams p,
 #pragma unroll
         for (int st = 0; st < 4; ++st) {
           const uint4 wq = *reinterpret_cast<const uint4*>(wst + woff[st]);
-          uint32_t mw[NSLOT];
+          uint32_t mw[NSLOT > 0 ? NSLOT : 1];
           if constexpr (KSEL > 0) {
 #pragma unroll
             for (int k = 0; k < KSEL; ++k) mw[k] = *reinterpret_cast<const uint32_t*>(wst + csel[k][st]);
-          } else
+          } else if constexpr (NM > 0)
 #pragma unroll
           for (int q = 0; q < (NM + 3) / 4; ++q) {
             // n_m = 8: the second 16-byte chunk is the next one in the swizzled span
@@ -312,11 +315,13 @@ gemv_mma_kernel(const DecParams p,
       for (int nb = 0; nb < NB; ++nb) {
         const int tok = nb * 4 + c;
         if (tok < B && row < nrows) {
-          float sv[NSLOT];
+          float sv[NSLOT > 0 ? NSLOT : 1];
 #pragma unroll
           for (int ii = 0; ii < NSLOT; ++ii) sv[ii] = 0.5f * (v[nb][0] + v[nb][1 + ii]);   // s_i = (t + u_i) / 2
           float y;
-          if constexpr (KSEL > 0) {                         // routed: slot k is mask sel[k], weight G
+          if constexpr (NM == 0) {
+            y = v[nb][0];                                   // dense projection x W (FFN W_o, row f1)
+          } else if constexpr (KSEL > 0) {                         // routed: slot k is mask sel[k], weight G
             y = 0.f;
             const float* gw = p.G + (size_t)tok * NM;
 #pragma unroll

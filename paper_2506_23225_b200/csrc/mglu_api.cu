@@ -201,7 +201,15 @@ bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, int rem_a, int re
   const int ra = rem_a ? rem_a : 1, rb = rem_b ? rem_b : 1;
   CUtensorMap m[6];
   const uint32_t fr = mglu::kDecFullRows;
-  bool ok =
+  if (NM == 0) {                                            // dense projection: W boxes only
+    const bool okd =
+        encode_3d_blocks(&m[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, fr, 4, sw) &&
+        encode_3d_blocks(&m[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, ra, 2 * wpt_of(rem_a), sw) &&
+        encode_3d_blocks(&m[4], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, rb, 2 * wpt_of(rem_b), sw);
+    if (!okd) return false;
+    m[1] = m[0]; m[3] = m[2]; m[5] = m[4];
+  }
+  bool ok = NM == 0 ||
       encode_3d_blocks(&m[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, fr, 4, sw) &&
       encode_3d_blocks(&m[1], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, fr, 2, csw) &&
       encode_3d_blocks(&m[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, ra, 2 * wpt_of(rem_a), sw) &&
@@ -252,7 +260,8 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   const size_t xbytes = (size_t)2 * (B + 1) * p.xpar * 4;   // + an all-zero token row
   const size_t partbytes = (size_t)mglu::kDecConsumers * 32 * NB * ((KSEL > 0 ? KSEL : NM) + 1) * 4;
   const size_t fixed = xbytes + partbytes + 1024;
-  const size_t cap = std::min<size_t>((size_t)hd->max_smem_optin, 200 * 1024);
+  // (dense handles with a long reduction stage a large x: let them use the whole opt-in budget)
+  const size_t cap = std::min<size_t>((size_t)hd->max_smem_optin, NM == 0 ? (size_t)hd->max_smem_optin : 200 * 1024);
   if (cap < fixed) return cudaErrorInvalidConfiguration;
   int S = (int)((cap - fixed) / (SB + 16));
   S = std::min(8, S);
@@ -303,6 +312,7 @@ cudaError_t mma_act(mglu_ctx* hd, const void* x, int B, const void* Wt, const vo
 cudaError_t mma_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes, void* out,
                    cudaStream_t st) {
   switch (hd->n_m) {
+    case 0: return run_mma<0, mglu::kIdentity>(hd, x, B, Wt, codes, out, st);   // dense projection
     case 1: return mma_act<1>(hd, x, B, Wt, codes, out, st);
     case 2: return mma_act<2>(hd, x, B, Wt, codes, out, st);
     case 4: return mma_act<4>(hd, x, B, Wt, codes, out, st);
@@ -313,7 +323,7 @@ cudaError_t mma_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const voi
 // ------------------------------------------------------------------ tcgen05 (prefill) dispatch
 bool tc_can_serve(const mglu_ctx* hd, int64_t B) {
   // TMA of the mask words: rows of d/32 * n_m u32 words must be 16-byte multiples
-  return hd->dtype == MGLU_BF16 && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 && B <= ((int64_t)1 << 31) - 1;
+  return hd->dtype == MGLU_BF16 && hd->n_m > 0 && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 && B <= ((int64_t)1 << 31) - 1;
 }
 
 // 2-D row-major [rows][cols] bf16 tensor, box [brows][bcols]
@@ -437,7 +447,7 @@ constexpr int kAutoMmaMaxB = 4, kAutoSkMaxB = 24;
 
 bool sk_can_serve(const mglu_ctx* hd, int64_t B) {
   // 64-column units; mask-word rows of d/32 * n_m u32 words must be 16-byte multiples (TMA)
-  return hd->dtype == MGLU_BF16 && hd->d % 64 == 0 && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 &&
+  return hd->dtype == MGLU_BF16 && hd->n_m > 0 && hd->d % 64 == 0 && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 &&
          B <= kSkMaxB && (hd->n_m < 8 || B <= 32);
 }
 
@@ -524,8 +534,8 @@ mglu_status check_ptrs(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, c
                        const void* out) {
   if (!hd) return MGLU_ERR_INVALID_ARG;
   if (B < 0) return set_err(hd, MGLU_ERR_INVALID_ARG, "B < 0");
-  if (!x || !Wt || !codes || !out) return set_err(hd, MGLU_ERR_INVALID_ARG, "null data pointer");
-  if (!aligned16(x) || !aligned16(Wt) || !aligned16(codes) || !aligned16(out))
+  if (!x || !Wt || (!codes && hd->n_m) || !out) return set_err(hd, MGLU_ERR_INVALID_ARG, "null data pointer");
+  if (!aligned16(x) || !aligned16(Wt) || (hd->n_m && !aligned16(codes)) || !aligned16(out))
     return set_err(hd, MGLU_ERR_MISALIGNED, "data pointers must be 16-byte aligned");
   if (B > (int64_t)1 << 30) return set_err(hd, MGLU_ERR_INVALID_ARG, "B too large");
   return MGLU_OK;
@@ -589,8 +599,9 @@ mglu_status mglu_create(mglu_handle* out, int64_t d, int64_t h, int n_m, int act
   *out = nullptr;
   if (d < 1 || h < 1 || act < 0 || act > 4 || (dtype != MGLU_BF16 && dtype != MGLU_F32) || device < 0)
     return MGLU_ERR_INVALID_ARG;
-  if (!valid_nm(n_m) || d % 32 != 0 || h > ((int64_t)1 << 31) - 1 || d > ((int64_t)1 << 24))
+  if ((!valid_nm(n_m) && n_m != 0) || d % 32 != 0 || h > ((int64_t)1 << 31) - 1 || d > ((int64_t)1 << 24))
     return MGLU_ERR_UNSUPPORTED;
+  if (n_m == 0 && dtype != MGLU_BF16) return MGLU_ERR_UNSUPPORTED;   // dense projection: bf16 MMA path
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) return MGLU_ERR_CUDA;
   cudaDeviceProp prop;
@@ -650,6 +661,11 @@ static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, con
   if (s != MGLU_OK) return s;
   hd->last_launches = 0;
   if (B == 0) return MGLU_OK;
+  if (hd->n_m == 0) {                                       // dense projection (FFN W_o): MMA path only
+    if (!mma_can_serve(hd, B) || (path != MGLU_PATH_AUTO && path != MGLU_PATH_MMA))
+      return set_err(hd, MGLU_ERR_UNSUPPORTED, "dense (n_m = 0) handles: MMA path, bf16, 1 <= B <= 8, d % 128 == 0");
+    path = MGLU_PATH_MMA;
+  }
   if (path == MGLU_PATH_AUTO) {
     // measured crossovers at the Llama-3-8B FFN shape (profiles/r01_paths_by_batch.txt): the
     // register-masked HMMA kernel for B <= 4 (one 8-column MMA tile), the stream-K tcgen05 GEMV for
@@ -795,7 +811,7 @@ mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, cons
 mglu_status mglu_forward_host(mglu_handle hd, const void* x_host, int64_t B, const void* Wt,
                               const void* packed, void* out_host, void* stream) {
   if (!hd) return MGLU_ERR_INVALID_ARG;
-  if (B < 0 || !x_host || !out_host || !Wt || !packed)
+  if (B < 0 || !x_host || !out_host || !Wt || (!packed && hd->n_m))
     return set_err(hd, MGLU_ERR_INVALID_ARG, "null pointer or B < 0");
   if (B == 0) return MGLU_OK;
   const size_t xb = (size_t)B * hd->d * elem_bytes(hd->dtype);

@@ -236,6 +236,8 @@ class Mglu:
             raise MgluError(MGLU_ERR_INVALID_ARG, f"x/Wt must be {td}")
         if tuple(Wt.shape) != (self.h, self.d) or x.shape[-1] != self.d:
             raise MgluError(MGLU_ERR_INVALID_ARG, "shape mismatch")
+        if self.n_m == 0 and packed is None:              # dense projection (FFN W_o): no codes
+            packed = torch.empty(0, dtype=torch.uint8, device=Wt.device)
         if packed.dtype != torch.uint8 or packed.numel() != mglu_packed_mask_bytes(self.d, self.h, self.n_m):
             raise MgluError(MGLU_ERR_INVALID_ARG, "packed codes size mismatch")
         if not (x.is_contiguous() and Wt.is_contiguous() and packed.is_contiguous()):
@@ -258,7 +260,7 @@ class Mglu:
         self._check_inputs(x, Wt, packed)
         lib = load_library()
         B = x.shape[0] if x.dim() == 2 else 1
-        args = (self.handle, x.data_ptr(), B, Wt.data_ptr(), packed.data_ptr(), out.data_ptr(),
+        args = (self.handle, x.data_ptr(), B, Wt.data_ptr(), packed.data_ptr() if packed is not None else None, out.data_ptr(),
                 _stream_ptr(stream, x.device))
         fwd = lib.mglu_forward
 

@@ -59,3 +59,27 @@ def gather_columns(y_local: torch.Tensor, h: int, group=None) -> torch.Tensor:
         lo, hi = shard_bounds(h, world, r)
         cols.append(parts[r][:, :hi - lo])
     return torch.cat(cols, dim=1)
+
+
+# ------------------------------------------------------------------ FFN block
+def shard_down(Wo: torch.Tensor, world: int, rank: int) -> torch.Tensor:
+    """Row-parallel (reduction-dim) shard of the down-projection Wo [d][h]: this rank's h-columns
+    [lo, hi) -- the rows of the up-projection it owns -- as a contiguous [d][hi - lo] copy (done
+    once at load time, as tensor-parallel frameworks store it)."""
+    lo, hi = shard_bounds(Wo.shape[1], world, rank)
+    return Wo[:, lo:hi].contiguous()
+
+
+def ffn_forward_tp(up, down, x: torch.Tensor, Wt_g: torch.Tensor, packed_g: torch.Tensor,
+                   Wo_g: torch.Tensor, group=None) -> torch.Tensor:
+    """One rank's SwiMGLU FFN block under tensor parallelism: the column-sharded up-projection
+    y_g = MGLU_g(x) [B][h_g] (no exchange), the row-sharded down-projection partial y_g Wo_g^T
+    [B][d] (an n_m = 0 dense handle), then ONE all-reduce (sum, fp32) of the partials over the
+    group -- the step's only collective (NCCL over NVLink on GPUs, gloo on CPU).  `up` / `down`
+    are Mglu handles of shapes (d, h_g, n_m) and (h_g, d, 0)."""
+    import torch.distributed as dist
+    y_g = up.forward(x, Wt_g, packed_g)
+    part = down.forward(y_g, Wo_g, None).float()
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+    return part

@@ -82,3 +82,34 @@ def test_gather_reassembles_full_output(tmp_path, world):
         y, ref = np.load(tmp_path / f"r{r}.npy")
         # columns are independent: the gathered shards equal the unsharded oracle exactly
         np.testing.assert_array_equal(y, ref)
+
+
+def _ffn_worker(rank, world, port, out_dir):
+    """Row f1 on CPU: rank-local oracle up-projection on the column shard, dense partial on the
+    W_o row shard, gloo all-reduce -- equals the unsharded FFN oracle."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import ACT_SWISH, decode_bf16, dense_np, ffn_forward_np, mglu_forward_np
+        from paper_2506_23225_b200.shard import shard_down
+        from synth import make_inputs
+        d, h, n_m, B = 64, 45, 2, 2
+        inp = make_inputs(21, B=B, d=d, h=h, n_m=n_m)
+        x, Wt = decode_bf16(inp["x"]), decode_bf16(inp["Wt"])
+        Wo = torch.from_numpy(np.random.default_rng(4).standard_normal((d, h)))
+        lo, hi = shard_bounds(h, world, rank)
+        y_g = mglu_forward_np(x, Wt[lo:hi], inp["bits"][:, lo:hi], ACT_SWISH)
+        part = torch.from_numpy(dense_np(y_g, shard_down(Wo, world, rank).numpy()))
+        dist.all_reduce(part, op=dist.ReduceOp.SUM)
+        ref = ffn_forward_np(x, Wt, inp["bits"], Wo.numpy(), ACT_SWISH)
+        np.save(os.path.join(out_dir, f"f{rank}.npy"), np.stack([part.numpy(), ref]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ffn_row_parallel_all_reduce(tmp_path, world):
+    mp.spawn(_ffn_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        out, ref = np.load(tmp_path / f"f{r}.npy")
+        np.testing.assert_allclose(out, ref, rtol=1e-12, atol=1e-12)
