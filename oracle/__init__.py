@@ -25,3 +25,4 @@ from . import accounting  # noqa: F401
 from .c_oracle import COracle, build_c_oracle  # noqa: F401
 from .topk import router_logits, topk_gate, mglu_routed_from_partials  # noqa: F401,E402
 from .ffn import ffn_forward_np, dense_np  # noqa: F401,E402
+from .variants import VARIANTS, mglu_variant_from_streams  # noqa: F401,E402
