@@ -501,7 +501,7 @@ def main(argv=None):
     ap.add_argument("--layers", type=int, default=4, help="distinct layer copies rotated (L2 hygiene)")
     ap.add_argument("--clock-window", type=float, default=0.3)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
-    ap.add_argument("--e2e-streams", type=int, default=2, help="streams the e2e (host-buffer) leg alternates over")
+    ap.add_argument("--e2e-streams", type=int, default=3, help="streams the e2e (host-buffer) leg alternates over")
     ap.add_argument("--topk", type=int, default=0, help="Top-K routed MGLU: K kept masks (router + routed forward)")
     ap.add_argument("--ffn", action="store_true", help="FFN block: up-projection + dense W_o (+ all-reduce under torchrun)")
     ap.add_argument("--no-comparator", action="store_true")

@@ -124,6 +124,13 @@ mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* W
 mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, const void* Wt,
                                   const void* packed, float* z, void* stream);
 
+/* Partial-mask ablation variants (PAPER.md "Partial Mask Ablation"):
+ * 0 = Eq. 3; 1 = NG (no gate mask: g(xW) (.) x(Mbar_i W)); 2 = NV (no value mask:
+ * g(x(M_i W)) (.) xW); 3 = NM (no masks: g(xW) (.) xW), each applied per mask term and summed over i
+ * (the paper defines n_m = 1).  Variants run on the MMA and SIMT paths (AUTO picks them); forcing a
+ * tcgen05 path with a variant set returns UNSUPPORTED.  Errors: INVALID_ARG (null, variant). */
+mglu_status mglu_set_variant(mglu_handle hd, int variant);
+
 /* Top-K routed MGLU (Appendix B).
  * mglu_router_topk: router logits l[b] = x[b] W_r in fp32 from bf16 inputs, then
  *   G[b] = Softmax(TopK(l[b])): the K largest logits (ties -> lowest index) get the

@@ -43,6 +43,21 @@ __device__ __forceinline__ float mglu_epilogue_w(float t, const float (&s)[NM], 
   return y;
 }
 
+// Partial-mask ablation variants (reading R20: per mask term): 1 NG gate = t,
+// 2 NV value = t, 3 NM both; 0 = Eq. 3.  Optional routed weights gw.
+template <int ACT, int NM>
+__device__ __forceinline__ float mglu_epilogue_v(float t, const float (&s)[NM], const float* gw, int variant) {
+  if (variant == 0) return mglu_epilogue_w<ACT, NM>(t, s, gw);
+  float y = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    const float gate = (variant & 1) ? t : s[i];
+    const float value = (variant & 2) ? t : t - s[i];
+    y = fmaf((gw ? gw[i] : 1.0f) * act_g<ACT>(gate), value, y);
+  }
+  return y;
+}
+
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 

@@ -57,6 +57,7 @@ struct DecParams {
   const __nv_bfloat16* x;
   __nv_bfloat16* out;
   const float* G;            // Top-K routed gate weights [B][n_m] (nullptr: plain Eq. 3)
+  int variant;               // partial-mask ablation variant (0 = Eq. 3; 1 NG, 2 NV, 3 NM)
   int B, d, h;
   int rows_base, rows_rem;   // CTA c owns rows_base + (c < rows_rem) rows
   int stages;                // ring depth
@@ -328,7 +329,7 @@ gemv_mma_kernel(const DecParams p,
             for (int k = 0; k < KSEL; ++k)
               if ((valid >> k) & 1u) y = fmaf(gw[sel[k]] * act_g<ACT>(sv[k]), v[nb][0] - sv[k], y);
           } else {
-            y = mglu_epilogue_w<ACT, NM>(v[nb][0], sv, p.G ? p.G + (size_t)tok * NM : nullptr);   // Eq. 3 (or all-mask routed)
+            y = mglu_epilogue_v<ACT, NM>(v[nb][0], sv, p.G ? p.G + (size_t)tok * NM : nullptr, p.variant);   // Eq. 3 / routed / variant
           }
           p.out[(size_t)tok * p.h + r0 + row] = __float2bfloat16_rn(y);
         }

@@ -28,6 +28,7 @@ struct mglu_ctx {
   int64_t d = 0, h = 0;
   int n_m = 0, act = 0, dtype = 0, device = 0;
   int path = MGLU_PATH_AUTO;
+  int variant = 0;           // partial-mask ablation variant (mglu_set_variant)
   int last_path = 0, last_launches = 0;
   int num_sms = 148;
   int max_smem_optin = 0;
@@ -114,7 +115,7 @@ cudaError_t run_simt(mglu_ctx* hd, const void* x, int B, const void* Wt, const v
   if (blocks > cap) blocks = cap;
   return launch_pdl(mglu::gemv_simt_kernel<T, NM, ACT, PARTIALS>, dim3((unsigned)blocks),
                     dim3(warps_per_block * 32), 0, st, (const T*)x, B, (int)hd->d, (const T*)Wt,
-                    (const uint8_t*)codes, (int)hd->h, (T*)out, z, t_routed_G);
+                    (const uint8_t*)codes, (int)hd->h, (T*)out, z, t_routed_G, hd->variant);
 }
 
 template <typename T, bool PARTIALS, int NM>
@@ -236,6 +237,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   p.x = (const __nv_bfloat16*)x;
   p.out = (__nv_bfloat16*)out;
   p.G = t_routed_G;
+  p.variant = hd->variant;
   p.B = B;
   p.d = (int)hd->d;
   p.h = (int)hd->h;
@@ -282,7 +284,7 @@ cudaError_t run_mma(mglu_ctx* hd, const void* x, int B, const void* Wt, const vo
   // token, so min(n_m, B*K) slots, rounded up to a power of two (other activations and larger
   // unions run all masks with the weights in the epilogue)
   if constexpr (ACT == mglu::kSwish && NM >= 2) {
-    if (t_routed_G && t_routed_K > 0) {
+    if (t_routed_G && t_routed_K > 0 && hd->variant == 0) {
       const int u = std::min(NM, B * t_routed_K);
       if (u <= 1) return B <= 4 ? run_mma_nb<NM, ACT, 1, 1>(hd, x, B, Wt, codes, out, st)
                                 : run_mma_nb<NM, ACT, 2, 1>(hd, x, B, Wt, codes, out, st);
@@ -648,6 +650,13 @@ mglu_status mglu_set_path(mglu_handle hd, int path) {
   return MGLU_OK;
 }
 
+mglu_status mglu_set_variant(mglu_handle hd, int variant) {
+  if (!hd || variant < 0 || variant > 3) return MGLU_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> g(hd->mu);
+  hd->variant = variant;
+  return MGLU_OK;
+}
+
 int mglu_last_launch_count(mglu_handle hd) { return hd ? hd->last_launches : -1; }
 int mglu_last_path(mglu_handle hd) { return hd ? hd->last_path : -1; }
 
@@ -665,6 +674,11 @@ static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, con
     if (!mma_can_serve(hd, B) || (path != MGLU_PATH_AUTO && path != MGLU_PATH_MMA))
       return set_err(hd, MGLU_ERR_UNSUPPORTED, "dense (n_m = 0) handles: MMA path, bf16, 1 <= B <= 8, d % 128 == 0");
     path = MGLU_PATH_MMA;
+  }
+  if (hd->variant != 0) {                                   // ablation variants: MMA / SIMT epilogues
+    if (path == MGLU_PATH_TCGEN05 || path == MGLU_PATH_TCDEC)
+      return set_err(hd, MGLU_ERR_UNSUPPORTED, "ablation variants run on the MMA or SIMT path");
+    if (path == MGLU_PATH_AUTO) path = mma_can_serve(hd, B) ? MGLU_PATH_MMA : MGLU_PATH_SIMT;
   }
   if (path == MGLU_PATH_AUTO) {
     // measured crossovers at the Llama-3-8B FFN shape (profiles/r01_paths_by_batch.txt): the

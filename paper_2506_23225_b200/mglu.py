@@ -58,6 +58,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "mglu_create": ([ctypes.POINTER(vp), i64, i64, c_int, c_int, c_int, c_int], c_int),
         "mglu_destroy": ([vp], c_int),
         "mglu_set_path": ([vp, c_int], c_int),
+        "mglu_set_variant": ([vp, c_int], c_int),
         "mglu_forward": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_forward_partials": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_forward_host": ([vp, vp, i64, vp, vp, vp, vp], c_int),
@@ -133,6 +134,13 @@ def mglu_destroy(handle: int) -> None:
 
 def mglu_set_path(handle: int, path: int) -> None:
     _check(load_library().mglu_set_path(handle, path), handle, "mglu_set_path")
+
+
+VARIANT = {"standard": 0, "no_gate_mask": 1, "no_value_mask": 2, "no_masks": 3}
+
+
+def mglu_set_variant(handle: int, variant: int) -> None:
+    _check(load_library().mglu_set_variant(handle, variant), handle, "mglu_set_variant")
 
 
 def mglu_forward(handle, x, B, Wt, packed, out, stream=None) -> None:
@@ -229,6 +237,10 @@ class Mglu:
 
     def set_path(self, path: str) -> None:
         mglu_set_path(self.handle, PATH[path])
+
+    def set_variant(self, variant: str) -> None:
+        """Partial-mask ablation variant: standard, no_gate_mask, no_value_mask, no_masks."""
+        mglu_set_variant(self.handle, VARIANT[variant])
 
     def _check_inputs(self, x, Wt, packed):
         td = TORCH_DTYPE[self.dtype]
