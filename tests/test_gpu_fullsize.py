@@ -84,3 +84,40 @@ def test_full_size_one_hot_decode():
         x[torch.arange(len(kk)), torch.tensor(kk)] = 1.0
         y = layer.forward(x, Wt, packed).float().cpu().numpy()
         np.testing.assert_array_equal(y, (n_m - pop[:, kk].T) / 2.0)
+
+
+PREFILL_FULL = [  # (name, d, h, n_m, B): the tensor-core workloads bench.py times, AUTO dispatch
+    ("config4_prefill", 8192, 28672, 4, 4096),
+    ("config5_b2048_nm8", 8192, 28672, 8, 2048),
+    ("config5_b2048_nm1", 8192, 28672, 1, 2048),
+    ("config3_b64", 4096, 14336, 4, 64),
+    ("config3_b16", 4096, 14336, 4, 16),
+]
+
+
+@pytest.mark.parametrize("name,d,h,n_m,B", PREFILL_FULL)
+def test_full_size_tensor_core_sampled(name, d, h, n_m, B):
+    """BASELINE configs 3 (B = 16, 64), 4 and 5 (B = 2048) at full size through AUTO (tcgen05 tile
+    GEMM / stream-K GEMV), device-drawn inputs as bench.py draws them; the oracle computes 48 sampled
+    tokens x 96 sampled output columns one by one (its own unpacker on the sampled rows)."""
+    from oracle import decode_bf16
+    from paper_2506_23225_b200.mglu import Mglu
+    from synth import random_packed_codes
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(B, d, device="cuda", generator=g).to(torch.bfloat16)
+    Wt = ((torch.rand(h, d, device="cuda", generator=g) * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+    packed = random_packed_codes(13 + n_m, h, d, n_m, device="cuda")
+    layer = Mglu(d, h, n_m, act="swish", dtype="bf16")
+    y = layer.forward(x, Wt, packed)
+    torch.cuda.synchronize()
+    assert layer.last_path() == ("tcdec" if B <= 24 else "tcgen05")
+    rng = np.random.default_rng(B + n_m)
+    toks = np.unique(np.concatenate([[0, B - 1], rng.choice(B, min(B, 46), replace=False)]))
+    cols = np.unique(np.concatenate([[0, 127, 128, h - 1], rng.choice(h, 92, replace=False)]))
+    ys = y[torch.from_numpy(toks).cuda()][:, torch.from_numpy(cols).cuda()].float().cpu().numpy().astype(np.float64)
+    xo = decode_bf16(x[torch.from_numpy(toks).cuda()].view(torch.int16).cpu().numpy().view(np.uint16))
+    Wo = decode_bf16(Wt[torch.from_numpy(cols).cuda()].view(torch.int16).cpu().numpy().view(np.uint16))
+    ref = oracle().forward(xo, Wo, cols, packed.cpu().numpy(), n_m, 1)
+    assert normwise_err(ys, ref) <= TIGHT["bf16"], name
+    del x, Wt, packed, y
+    torch.cuda.empty_cache()
