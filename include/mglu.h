@@ -127,8 +127,8 @@ mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, cons
 /* Partial-mask ablation variants (PAPER.md "Partial Mask Ablation"):
  * 0 = Eq. 3; 1 = NG (no gate mask: g(xW) (.) x(Mbar_i W)); 2 = NV (no value mask:
  * g(x(M_i W)) (.) xW); 3 = NM (no masks: g(xW) (.) xW), each applied per mask term and summed over i
- * (the paper defines n_m = 1).  Variants run on the MMA and SIMT paths (AUTO picks them); forcing a
- * tcgen05 path with a variant set returns UNSUPPORTED.  Errors: INVALID_ARG (null, variant). */
+ * (the paper defines n_m = 1).  Every path applies the variant in its epilogue.
+ * Errors: INVALID_ARG (null, variant). */
 mglu_status mglu_set_variant(mglu_handle hd, int variant);
 
 /* Top-K routed MGLU (Appendix B).
@@ -144,8 +144,8 @@ mglu_status mglu_set_variant(mglu_handle hd, int variant);
  *   produced by mglu_router_topk with that K); 0 = no promise.  With K > 0 the MMA path evaluates
  *   only the masks some token of the call selected (at most min(n_m, B*K); their sign flips and MMAs,
  *   Swish only -- other activations evaluate every mask); a G violating the promise gives undefined
- *   output.  Runs the MMA path (bf16, B <= 8) or the SIMT path; forcing TCGEN05/TCDEC returns
- *   UNSUPPORTED in this version.  Errors as mglu_forward, plus INVALID_ARG (K) / MISALIGNED for G. */
+ *   output.  Dispatch as mglu_forward (the tensor-core paths evaluate every mask and weigh them in
+ *   their epilogues).  Errors as mglu_forward, plus INVALID_ARG (K) / MISALIGNED for G. */
 mglu_status mglu_router_topk(mglu_handle hd, const void* x, int64_t B, const void* Wr, int K, float* G,
                              void* stream);
 mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* packed,

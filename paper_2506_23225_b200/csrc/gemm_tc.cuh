@@ -64,6 +64,8 @@ static_assert(tc_tmem_used<1>() <= 512 && tc_tmem_used<2>() <= 512 && tc_tmem_us
 
 struct TcParams {
   __nv_bfloat16* out;        // [B][h]
+  const float* G;            // Top-K routed gate weights [B][n_m] (nullptr: every weight 1)
+  int variant;               // partial-mask ablation variant (0 = Eq. 3)
   int B, d, h;
   int stages;
 };
@@ -248,11 +250,15 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float t = __uint_as_float(tv[q]);
+        const int tq = n0 + c0 + q;                        // token of this column
         float acc = 0.f;
 #pragma unroll
         for (int i = 0; i < MPC; ++i) {
           const float sg = 0.5f * (t + __uint_as_float(uv[i][q]));       // s_i = (t + u_i) / 2
-          acc = fmaf(act_g<ACT>(sg), t - sg, acc);                        // g(s_i) (t - s_i)
+          const float gate = (p.variant & 1) ? t : sg;                    // ablation variants
+          const float value = (p.variant & 2) ? t : t - sg;
+          const float wgt = p.G ? (tq < p.B ? p.G[(size_t)tq * NM + moff + i] : 0.f) : 1.f;   // routed (App. B)
+          acc = fmaf(wgt * act_g<ACT>(gate), value, acc);                 // g(s_i) (t - s_i)
         }
         yp[ch][q] = acc;
       }

@@ -53,6 +53,8 @@ constexpr int kSkKS = MGLU_SK_KS;   // reduction columns per unit (= shared-memo
 
 struct SkParams {
   __nv_bfloat16* out;   // [B][h]
+  const float* G;       // Top-K routed gate weights [B][n_m] (nullptr: every weight 1)
+  int variant;          // partial-mask ablation variant (0 = Eq. 3)
   float* ws;            // partials [gridDim.x][NOP][B][128]
   uint32_t* flags;      // [gridDim.x], 0 between calls
   int B, d, h, act;
@@ -335,7 +337,10 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
 #pragma unroll
               for (int i = 0; i < NM; ++i) {
                 const float sg = 0.5f * (t + f[1 + i][q]);
-                y = fmaf(act_rt(p.act, sg), t - sg, y);
+                const float gate = (p.variant & 1) ? t : sg;                // ablation variants
+                const float value = (p.variant & 2) ? t : t - sg;
+                const float wgt = p.G ? p.G[(size_t)tok * NM + i] : 1.f;    // routed (Appendix B)
+                y = fmaf(wgt * act_rt(p.act, gate), value, y);
               }
               p.out[(size_t)tok * p.h + grow] = __float2bfloat16_rn(y);
             }

@@ -378,6 +378,8 @@ cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
     return cudaErrorInvalidValue;
   mglu::TcParams p;
   p.out = (__nv_bfloat16*)out;
+  p.G = t_routed_G;
+  p.variant = hd->variant;
   p.B = (int)B;
   p.d = (int)hd->d;
   p.h = (int)hd->h;
@@ -481,6 +483,8 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
     return cudaErrorInvalidValue;
   mglu::SkParams p;
   p.out = (__nv_bfloat16*)out;
+  p.G = t_routed_G;
+  p.variant = hd->variant;
   p.B = (int)B;
   p.d = (int)hd->d;
   p.h = (int)hd->h;
@@ -675,11 +679,6 @@ static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, con
       return set_err(hd, MGLU_ERR_UNSUPPORTED, "dense (n_m = 0) handles: MMA path, bf16, 1 <= B <= 8, d % 128 == 0");
     path = MGLU_PATH_MMA;
   }
-  if (hd->variant != 0) {                                   // ablation variants: MMA / SIMT epilogues
-    if (path == MGLU_PATH_TCGEN05 || path == MGLU_PATH_TCDEC)
-      return set_err(hd, MGLU_ERR_UNSUPPORTED, "ablation variants run on the MMA or SIMT path");
-    if (path == MGLU_PATH_AUTO) path = mma_can_serve(hd, B) ? MGLU_PATH_MMA : MGLU_PATH_SIMT;
-  }
   if (path == MGLU_PATH_AUTO) {
     // measured crossovers at the Llama-3-8B FFN shape (profiles/r01_paths_by_batch.txt): the
     // register-masked HMMA kernel for B <= 4 (one 8-column MMA tile), the stream-K tcgen05 GEMV for
@@ -790,10 +789,8 @@ mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const 
     std::lock_guard<std::mutex> g(hd->mu);
     path = hd->path;
   }
-  if (path == MGLU_PATH_TCGEN05 || path == MGLU_PATH_TCDEC)
-    return set_err(hd, MGLU_ERR_UNSUPPORTED, "routed forward: MMA or SIMT paths only (round 1)");
-  // the routed weights reach the MMA / SIMT launchers through a thread-local pointer
-  if (path == MGLU_PATH_AUTO) path = mma_can_serve(hd, B) ? MGLU_PATH_MMA : MGLU_PATH_SIMT;
+  // the routed weights reach every launcher through a thread-local pointer; the MMA path also skips
+  // the masks no token selected, the tensor-core paths weigh every mask in their epilogues
   t_routed_G = G;
   t_routed_K = K;
   s = forward_on_path(hd, x, B, Wt, packed, out, stream, path);

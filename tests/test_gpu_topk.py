@@ -61,7 +61,7 @@ def test_router_matches_oracle(n_m, K, B):
     assert np.allclose(G.sum(axis=1), 1.0, atol=1e-6)
 
 
-@pytest.mark.parametrize("path", ["mma", "simt"])
+@pytest.mark.parametrize("path", ["mma", "simt", "tcdec", "tcgen05"])
 @pytest.mark.parametrize("n_m,K,B", [(4, 1, 1), (4, 2, 3), (8, 2, 1), (8, 3, 5), (8, 8, 8), (2, 1, 2), (8, 1, 2),
                                      (8, 4, 1), (8, 2, 2)])
 def test_routed_forward_matches_oracle(path, n_m, K, B):
@@ -118,20 +118,36 @@ def test_router_then_routed_forward_chain():
 
 
 def test_routed_errors():
-    from paper_2506_23225_b200.mglu import Mglu, MgluError, MGLU_ERR_INVALID_ARG, MGLU_ERR_UNSUPPORTED
+    from paper_2506_23225_b200.mglu import Mglu, MgluError, MGLU_ERR_INVALID_ARG
     d, h, n_m = 512, 256, 4
     layer = Mglu(d, h, n_m, dtype="bf16")
     x = torch.zeros(1, d, dtype=torch.bfloat16, device="cuda")
     Wr = torch.zeros(n_m, d, dtype=torch.bfloat16, device="cuda")
-    with pytest.raises(MgluError) as e:
-        layer.router_topk(x, Wr, 0)
-    assert e.value.status == MGLU_ERR_INVALID_ARG
-    with pytest.raises(MgluError) as e:
-        layer.router_topk(x, Wr, n_m + 1)
-    assert e.value.status == MGLU_ERR_INVALID_ARG
-    layer.set_path("tcgen05")
+    for K in (0, n_m + 1):
+        with pytest.raises(MgluError) as e:
+            layer.router_topk(x, Wr, K)
+        assert e.value.status == MGLU_ERR_INVALID_ARG
     Wt = torch.zeros(h, d, dtype=torch.bfloat16, device="cuda")
     packed = torch.zeros(h * d * n_m // 8, dtype=torch.uint8, device="cuda")
     with pytest.raises(MgluError) as e:
-        layer.forward_routed(x, Wt, packed, torch.zeros(1, n_m, device="cuda"), 1)
-    assert e.value.status == MGLU_ERR_UNSUPPORTED
+        layer.forward_routed(x, Wt, packed, torch.zeros(1, n_m, device="cuda"), n_m + 1)
+    assert e.value.status == MGLU_ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("B", [40, 300])
+def test_routed_forward_large_batch_auto(B):
+    """Prefill-sized routed batches through AUTO (stream-K GEMV / tcgen05 tile GEMM: every mask
+    evaluated, weighted in the epilogue)."""
+    from oracle import topk_gate
+    from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
+    d, h, n_m, K = 1024, 512, 4, 2
+    inp = make_inputs(1000 + B, B=B, d=d, h=h, n_m=n_m, dtype="bf16")
+    x, Wt = to_device(inp, "bf16")
+    packed = torch.from_numpy(mglu_pack_masks_host(inp["bits"])).cuda()
+    G = topk_gate(np.random.default_rng(B).standard_normal((B, n_m)), K).astype(np.float32)
+    layer = Mglu(d, h, n_m, act="swish", dtype="bf16")
+    y = layer.forward_routed(x, Wt, packed, torch.from_numpy(G).cuda(), K)
+    torch.cuda.synchronize()
+    assert layer.last_path() == ("tcdec" if B <= 24 else "tcgen05")
+    ref = _oracle_routed(inp, n_m, 1, G.astype(np.float64))
+    assert normwise_err(y.float().cpu().numpy().astype(np.float64), ref) <= TIGHT["bf16"]
