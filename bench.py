@@ -142,13 +142,18 @@ def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # (MGLU_DIST_BACKEND=gloo runs several ranks on one GPU: exercises the multi-rank code, its
+    # timings are not bench numbers)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
-    return ws, rank, local
+        backend = os.environ.get("MGLU_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    return ws, rank, dev
 
 
 def barrier(ws):
@@ -246,6 +251,7 @@ def cpu_baseline(d, h, n_m, B, act_code, budget_s=10.0):
     work; the rate is scaled to the metric's unit from the columns actually computed."""
     from oracle import COracle
     o = COracle()
+    o.set_num_threads(os.cpu_count() or 1)
     rng = np.random.default_rng(0)
     c = oracle_sample_cols(d, h, n_m, B)
     x = rng.standard_normal((B, d))
@@ -276,6 +282,9 @@ def run_reference(args, ws, rank):
     from oracle import ACT_NAMES, COracle
     d, h, n_m, B, act, desc = WORKLOADS[args.workload]
     o = COracle()
+    # torchrun sets OMP_NUM_THREADS=1 per process; rank 0 is the only rank working here, so the
+    # oracle gets the host's cores (its result does not depend on the thread count)
+    o.set_num_threads(os.cpu_count() or 1)
     rng = np.random.default_rng(0)
     c = oracle_sample_cols(d, h, n_m, B)
     x = rng.standard_normal((B, d))
@@ -362,15 +371,19 @@ def run_mglu(args, ws, rank, local):
         stream.synchronize()
         launches_per_step = layer.last_launch_count() + (1 if (args.topk or args.ffn) else 0)
         path_used = layer.last_path()
-        # clock window + timed region, NVML-sampled
+        # clock window + timed region, NVML-sampled.  The window is a step COUNT agreed by all ranks
+        # (steps may hold collectives: every rank must run the same number)
+        t0 = time.perf_counter()
+        for k in range(args.warmup):
+            step(k)
+        stream.synchronize()
+        t_step = max_over_ranks(ws, (time.perf_counter() - t0) / max(1, args.warmup))
+        n_clock = int(min(100000, args.clock_window / max(t_step, 1e-7)))
         sampler = ClockSampler(local)
         sampler.start()
-        t_end = time.perf_counter() + args.clock_window
-        k = 0
-        while time.perf_counter() < t_end:
+        for k in range(n_clock):
             step(k)
-            k += 1
-            if k % 256 == 0:
+            if (k + 1) % 256 == 0:
                 stream.synchronize()
         stream.synchronize()
         barrier(ws)

@@ -46,10 +46,14 @@ class COracle:
                                             ctypes.c_int64, _u8p, ctypes.c_int, ctypes.c_int,
                                             _dp, _dp, _dp]
         lib.oracle_num_threads.restype = ctypes.c_int
+        lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
         self.lib = lib
 
     def num_threads(self) -> int:
         return int(self.lib.oracle_num_threads())
+
+    def set_num_threads(self, n: int) -> None:
+        self.lib.oracle_set_num_threads(int(n))
 
     def pack(self, bits: np.ndarray) -> np.ndarray:
         bits = np.ascontiguousarray(bits, dtype=np.uint8)

@@ -70,6 +70,16 @@ static double act_g(int act, double z) {
     }
 }
 
+/* thread count of the column loop (the result does not depend on it: each output column is one
+   sequential k loop) -- lets a benchmark that runs under torchrun (OMP_NUM_THREADS=1) use the host */
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();
