@@ -34,7 +34,13 @@ template <> struct TcCfg<2> { static constexpr int BN = 128, KA = 32, MPC = 2; }
 #ifndef MGLU_TC_KA4
 #define MGLU_TC_KA4 32
 #endif
-template <> struct TcCfg<4> { static constexpr int BN = 64, KA = MGLU_TC_KA4, MPC = 4; };
+#ifndef MGLU_TC_ODD_SLOTS
+#define MGLU_TC_ODD_SLOTS 0
+#endif
+#ifndef MGLU_TC_BN4
+#define MGLU_TC_BN4 64
+#endif
+template <> struct TcCfg<4> { static constexpr int BN = MGLU_TC_BN4, KA = MGLU_TC_KA4, MPC = 4; };
 template <> struct TcCfg<8> { static constexpr int BN = 64, KA = 32, MPC = 4; };
 
 constexpr int kTcThreads = 320;
@@ -43,7 +49,9 @@ constexpr int kTcK = 64;                        // reduction columns per shared 
 // TMEM A slots: 4 when the accumulators leave room (small token tiles: deeper masker run-ahead
 // hides the slot round trip), else 2 -- always even, so every slot belongs to one masker group
 template <int NM, int BN> __host__ __device__ constexpr int tc_slots() {
-  return (TcCfg<NM>::MPC + 1) * BN + 4 * (TcCfg<NM>::MPC + 1) * TcCfg<NM>::KA / 2 <= 512 ? 4 : 2;
+  constexpr int acc = (TcCfg<NM>::MPC + 1) * BN, slot = (TcCfg<NM>::MPC + 1) * TcCfg<NM>::KA / 2;
+  constexpr int fit = (512 - acc) / slot;
+  return fit >= 4 ? 4 : (MGLU_TC_ODD_SLOTS && fit == 3) ? 3 : 2;
 }
 
 // mask words per row per stage as loaded by TMA: 2 groups x n_m words, at least 16 bytes
