@@ -43,13 +43,11 @@
 
 namespace mglu {
 
-#ifndef MGLU_SK_KS
-#define MGLU_SK_KS 256
-#endif
-#ifndef MGLU_SK_KA
-#define MGLU_SK_KA 32
-#endif
-constexpr int kSkKS = MGLU_SK_KS;   // reduction columns per unit (= shared-memory stage)
+// reduction columns per unit (= shared-memory stage) and per TMEM A-stage, by mask count (measured,
+// profiles/r01_tcdec_experiments.txt: 256 / 64 for n_m <= 4; n_m = 8 keeps its stages small,
+// 128 / 16, for ring depth and TMEM room)
+template <int NM> __host__ __device__ constexpr int sk_ks() { return NM == 8 ? 128 : 256; }
+template <int NM> __host__ __device__ constexpr int sk_ka() { return NM == 8 ? 16 : 64; }
 
 struct SkParams {
   __nv_bfloat16* out;   // [B][h]
@@ -89,20 +87,21 @@ __device__ __forceinline__ float act_rt(int act, float z) {
 // geometry of one instantiation: NM masks, BN token columns, MG masker groups of 4 warps
 template <int NM, int BN, int MG> struct SkCfg {
   static constexpr int NOP = NM + 1;
-  static constexpr int KA = NM == 8 ? 16 : MGLU_SK_KA;
+  static constexpr int KS = sk_ks<NM>();
+  static constexpr int KA = sk_ka<NM>();
   static constexpr int SLOT = NOP * KA / 2;
   static constexpr int ACC = NOP * BN;
   static constexpr int NACC = 2 * ACC + 2 * MG * SLOT <= 512 ? 2 : 1;
   static constexpr int SA_FIT = (512 - NACC * ACC) / SLOT / MG * MG;
   static constexpr int SA = SA_FIT > 4 * MG ? 4 * MG : SA_FIT;
-  static constexpr int WPS = kSkKS / 32 * NM;
+  static constexpr int WPS = KS / 32 * NM;
   static constexpr int CW = WPS < 4 ? 4 : WPS;
-  static constexpr int WB = kSkKS / 64 * 128 * 128;
-  static constexpr int XB = kSkKS / 64 * BN * 128;
+  static constexpr int WB = KS / 64 * 128 * 128;
+  static constexpr int XB = KS / 64 * BN * 128;
   static constexpr int CB = 128 * CW * 4;
   static constexpr int SB = (WB + XB + CB + 1023) / 1024 * 1024;
   static constexpr int THREADS = (4 * MG + 6) * 32;
-  static constexpr bool ok = SA >= MG && kSkKS / KA >= MG && (kSkKS / KA) % MG == 0;
+  static constexpr bool ok = SA >= MG && KS / KA >= MG && (KS / KA) % MG == 0;
 };
 
 template <int NM, int BN, int MG>
@@ -112,7 +111,7 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
   using C = SkCfg<NM, BN, MG>;
   constexpr int NOP = C::NOP, KA = C::KA, SLOT = C::SLOT, SA = C::SA, NACC = C::NACC, ACC = C::ACC;
   constexpr int WPS = C::WPS, CW = C::CW, WB = C::WB, XB = C::XB, SB = C::SB;
-  constexpr int APS = kSkKS / KA, WW = KA / 2;
+  constexpr int KS = C::KS, APS = KS / KA, WW = KA / 2;
   constexpr uint32_t IDESC = idesc_bf16_f32(128, BN);
   constexpr uint32_t A_COL0 = NACC * ACC;
   constexpr int kTma = 4 * MG, kMma = 4 * MG + 1, kEpi0 = 4 * MG + 2;
@@ -161,13 +160,13 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
         const int u = u0 + i, tile = u / upt, ks = u - tile * upt;
         uint8_t* st = smem + (size_t)i * SB;
         mbar_arrive_expect_tx(&full[i], (uint32_t)(WB + XB + C::CB));
-        tma_load_3d_hint(st, &mW, 0, tile * 128, ks * (kSkKS / 64), &full[i], pol);
+        tma_load_3d_hint(st, &mW, 0, tile * 128, ks * (KS / 64), &full[i], pol);
         tma_load_2d_hint(st + WB + XB, &mC, (ks * WPS) / CW * CW, tile * 128, &full[i], pol);
       }
       pdl_wait();
       for (int i = 0; i < pre; ++i) {
         const int ks = (u0 + i) % upt;
-        tma_load_3d(smem + (size_t)i * SB + WB, &mX, 0, 0, ks * (kSkKS / 64), &full[i]);
+        tma_load_3d(smem + (size_t)i * SB + WB, &mX, 0, 0, ks * (KS / 64), &full[i]);
       }
       int s = pre % S;
       uint32_t ph = pre == S ? 1u : 0u;
@@ -176,8 +175,8 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* st = smem + (size_t)s * SB;
         mbar_arrive_expect_tx(&full[s], (uint32_t)(WB + XB + C::CB));
-        tma_load_3d_hint(st, &mW, 0, tile * 128, ks * (kSkKS / 64), &full[s], pol);
-        tma_load_3d(st + WB, &mX, 0, 0, ks * (kSkKS / 64), &full[s]);
+        tma_load_3d_hint(st, &mW, 0, tile * 128, ks * (KS / 64), &full[s], pol);
+        tma_load_3d(st + WB, &mX, 0, 0, ks * (KS / 64), &full[s]);
         tma_load_2d_hint(st + WB + XB, &mC, (ks * WPS) / CW * CW, tile * 128, &full[s], pol);
         if (++s == S) { s = 0; ph ^= 1; }
       }
@@ -242,8 +241,12 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
           const uint4 v = *reinterpret_cast<const uint4*>(st + (col >> 6) * 16384 + m * 128 + chunk * 16);
           w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
         }
-        uint32_t cw[NM];                                   // (swizzled code box: conflict-free reads)
-        lds_words_swz<NM>(st + WB + XB, (uint32_t)(m * CW * 4 + (wofs + (col >> 5) * NM) * 4), CW * 4, cw);
+        // mask words of the A-stage's 32-column groups (swizzled code box: conflict-free reads)
+        constexpr int NG = KA >= 32 ? KA / 32 : 1, PPG = KA >= 32 ? 16 : KA / 2;
+        uint32_t cw[NG][NM];
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi)
+          lds_words_swz<NM>(st + WB + XB, (uint32_t)(m * CW * 4 + (wofs + ((col >> 5) + gi) * NM) * 4), CW * 4, cw[gi]);
         const int pair0 = (col & 31) >> 1;
         const int sa = js % SA;
         mbar_wait(&a_empty[sa], ((uint32_t)(js / SA) & 1u) ^ 1u);
@@ -254,7 +257,8 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
         for (int i = 0; i < NM; ++i) {
           uint32_t op[WW];
 #pragma unroll
-          for (int q = 0; q < WW; ++q) op[q] = sign_flip(w[q], cw[i], 1u << (15 - pair0 - q));
+          for (int q = 0; q < WW; ++q)                     // pair q: group q / PPG, bits (p, p + 16)
+            op[q] = sign_flip(w[q], cw[q / PPG][i], 1u << (15 - pair0 - (q % PPG)));
           tmem_st_n<WW>(a0 + (uint32_t)((1 + i) * WW), op);
         }
         tmem_st_wait();

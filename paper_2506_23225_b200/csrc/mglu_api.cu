@@ -476,7 +476,7 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   using C = mglu::SkCfg<NM, BN, MG>;
   CUtensorMap mW, mX, mC;
   const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
-  constexpr int KB = mglu::kSkKS / 64;
+  constexpr int KB = C::KS / 64;
   if (!encode_3d_blocks(&mW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, 128, KB, sw) ||
       !encode_3d_blocks(&mX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, hd->d, B, 64, BN, KB, sw) ||
       !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, C::CW, 128, code_swizzle(C::CW * 4)))
@@ -489,7 +489,7 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   p.d = (int)hd->d;
   p.h = (int)hd->h;
   p.act = hd->act;
-  p.upt = (int)((hd->d + mglu::kSkKS - 1) / mglu::kSkKS);   // a final half unit reads zero-filled boxes
+  p.upt = (int)((hd->d + C::KS - 1) / C::KS);   // a final partial unit reads zero-filled boxes
   const int64_t units = (hd->h + 127) / 128 * p.upt;
   const int64_t G = std::min<int64_t>(hd->num_sms, units);
   p.units_base = (int)(units / G);
