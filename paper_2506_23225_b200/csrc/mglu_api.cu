@@ -683,7 +683,11 @@ static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, con
     // measured crossovers at the Llama-3-8B FFN shape (profiles/r01_paths_by_batch.txt): the
     // register-masked HMMA kernel for B <= 4 (one 8-column MMA tile), the stream-K tcgen05 GEMV for
     // 5 <= B <= 24, the tcgen05 tile GEMM above; SIMT for fp32 and shapes the others refuse
-    if (B <= kAutoMmaMaxB && mma_can_serve(hd, B))
+    // (n_m = 8 on large layers: the HMMA kernel's 9 MMAs per step make it compute-bound, and the
+    //  tcgen05 GEMV wins from B = 1: 151 vs 161 us at d=8192 h=28672, 41.5 vs 43.7 at the config-3
+    //  shape; on small shards (h < 8192) the HMMA kernel stays ahead)
+    const bool nm8_big = hd->n_m == 8 && hd->h >= 8192 && sk_can_serve(hd, B);
+    if (B <= kAutoMmaMaxB && mma_can_serve(hd, B) && !nm8_big)
       path = MGLU_PATH_MMA;
     else if (B <= kAutoSkMaxB && sk_can_serve(hd, B))
       path = MGLU_PATH_TCDEC;
@@ -791,6 +795,7 @@ mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const 
   }
   // the routed weights reach every launcher through a thread-local pointer; the MMA path also skips
   // the masks no token selected, the tensor-core paths weigh every mask in their epilogues
+  if (path == MGLU_PATH_AUTO && K > 0 && mma_can_serve(hd, B)) path = MGLU_PATH_MMA;   // it skips masks
   t_routed_G = G;
   t_routed_K = K;
   s = forward_on_path(hd, x, B, Wt, packed, out, stream, path);
