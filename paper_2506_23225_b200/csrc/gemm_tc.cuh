@@ -48,8 +48,12 @@ constexpr int kTcMaskWarps = 8;
 constexpr int kTcK = 64;                        // reduction columns per shared stage
 // TMEM A slots: 4 when the accumulators leave room (small token tiles: deeper masker run-ahead
 // hides the slot round trip), else 2 -- always even, so every slot belongs to one masker group
+#ifndef MGLU_TC_SS_T
+#define MGLU_TC_SS_T 0   // 1: t's MMA reads W straight from shared memory (SS); slots hold the masked copies only
+#endif
+template <int NM> __host__ __device__ constexpr int tc_slot_ops() { return TcCfg<NM>::MPC + (MGLU_TC_SS_T ? 0 : 1); }
 template <int NM, int BN> __host__ __device__ constexpr int tc_slots() {
-  constexpr int acc = (TcCfg<NM>::MPC + 1) * BN, slot = (TcCfg<NM>::MPC + 1) * TcCfg<NM>::KA / 2;
+  constexpr int acc = (TcCfg<NM>::MPC + 1) * BN, slot = tc_slot_ops<NM>() * TcCfg<NM>::KA / 2;
   constexpr int fit = (512 - acc) / slot;
   return fit >= 4 ? 4 : (MGLU_TC_ODD_SLOTS && fit == 3) ? 3 : 2;
 }
@@ -83,7 +87,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mW,
                const __grid_constant__ CUtensorMap mC) {
   constexpr int KA = TcCfg<NM>::KA, SA = tc_slots<NM, BN>();
-  static_assert((TcCfg<NM>::MPC + 1) * BN + SA * (TcCfg<NM>::MPC + 1) * KA / 2 <= 512, "TMEM budget");
+  constexpr int NSL = tc_slot_ops<NM>();                  // operands stored per A slot
+  constexpr int SS = MGLU_TC_SS_T;                         // t from shared memory
+  static_assert((TcCfg<NM>::MPC + 1) * BN + SA * NSL * KA / 2 <= 512, "TMEM budget");
   constexpr int MPC = TcCfg<NM>::MPC, NSPLIT = tc_split<NM>();
   constexpr int NOP = MPC + 1;                             // operands: W and this CTA's sign-flipped copies
   constexpr int XB = tc_x_bytes<BN>(), WB = 128 * kTcK * 2, CW = tc_code_words<NM>();
@@ -170,10 +176,14 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
           }
           if (elect_one()) {
             const uint64_t bdesc = bdesc_s + (uint64_t)(kk * 2);          // +32 bytes along K
-            const uint32_t a0 = tmem + A_COL0 + (uint32_t)(sa * NOP * WW + (kk % KPS) * 8);
+            const uint32_t a0 = tmem + A_COL0 + (uint32_t)(sa * NSL * WW + (kk % KPS) * 8);
             const uint32_t acc = j > 0 ? 1u : 0u;
+            if constexpr (SS) {
+              const uint64_t adesc = smem_desc_kmajor(smem_u32(smem) + XB, 128) + (uint64_t)((s * SB) >> 4) + (uint64_t)(kk * 2);
+              tc_mma_ss(tmem, adesc, bdesc, IDESC, acc);                                 // t: W from smem
+            }
 #pragma unroll
-            for (int op = 0; op < NOP; ++op) tc_mma_ts(tmem + op * BN, a0 + op * WW, bdesc, IDESC, acc);
+            for (int op = SS; op < NOP; ++op) tc_mma_ts(tmem + op * BN, a0 + (op - SS) * WW, bdesc, IDESC, acc);
             if (kk % KPS == KPS - 1) tc_commit(&a_empty[sa]);
           }
           __syncwarp();
@@ -227,11 +237,11 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
         const int sa = js % SA;
         mbar_wait(&a_empty[sa], ((uint32_t)(js / SA) & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t a0 = a_lane + (uint32_t)(sa * NOP * WW);
+        const uint32_t a0 = a_lane + (uint32_t)(sa * NSL * WW);
 #pragma unroll
-        for (int o = 0; o < NOP; ++o) {
-          if constexpr (WW == 16) tmem_st16(a0 + o * WW, op[o]);
-          else tmem_st8(a0 + o * WW, *reinterpret_cast<uint32_t(*)[8]>(&op[o][0]));
+        for (int o = SS; o < NOP; ++o) {
+          if constexpr (WW == 16) tmem_st16(a0 + (o - SS) * WW, op[o]);
+          else tmem_st8(a0 + (o - SS) * WW, *reinterpret_cast<uint32_t(*)[8]>(&op[o][0]));
         }
         tmem_st_wait();
         tc_fence_before();
