@@ -90,7 +90,7 @@ int oracle_num_threads(void) {
 
 /* bits[(i-1)][j][k] in {0,1}  ->  packed layout (h*d*n_m/8 bytes) */
 int oracle_pack(const uint8_t *bits, int n_m, int64_t h, int64_t d, uint8_t *packed) {
-    if (n_m < 1 || n_m > 8 || h < 0 || d < 0 || d % 32) return 1;
+    if (n_m < 1 || n_m > 16 || h < 0 || d < 0 || d % 32) return 1;
     memset(packed, 0, (size_t)((uint64_t)n_m * (uint64_t)h * (uint64_t)d / 8u));
     for (int64_t j = 0; j < h; ++j)
         for (int64_t k = 0; k < d; ++k)
@@ -105,7 +105,7 @@ int oracle_pack(const uint8_t *bits, int n_m, int64_t h, int64_t d, uint8_t *pac
 
 /* packed layout -> bits[(i-1)][j][k] */
 int oracle_unpack(const uint8_t *packed, int n_m, int64_t h, int64_t d, uint8_t *bits) {
-    if (n_m < 1 || n_m > 8 || h < 0 || d < 0 || d % 32) return 1;
+    if (n_m < 1 || n_m > 16 || h < 0 || d < 0 || d % 32) return 1;
     for (int i = 1; i <= n_m; ++i)
         for (int64_t j = 0; j < h; ++j)
             for (int64_t k = 0; k < d; ++k)
@@ -128,7 +128,7 @@ int oracle_mglu_forward(const double *x, int64_t B, int64_t d,
                         const double *Wt_sel, const int64_t *cols, int64_t ncols,
                         const uint8_t *packed, int n_m, int act,
                         double *y, double *z, double *t_out) {
-    if (n_m < 1 || n_m > 8 || act < 0 || act > 4 || B < 0 || d < 0 || d % 32 || ncols < 0) return 1;
+    if (n_m < 1 || n_m > 16 || act < 0 || act > 4 || B < 0 || d < 0 || d % 32 || ncols < 0) return 1;
     int64_t c;
 #pragma omp parallel for schedule(dynamic, 8)
     for (c = 0; c < ncols; ++c) {

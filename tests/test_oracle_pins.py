@@ -327,3 +327,26 @@ def test_layout_bit_positions(c_oracle, n_m):
                 want[i, 0, 32 * g + 2 * (pbit % 16) + pbit // 16] = 1
                 np.testing.assert_array_equal(unpack_np(packed, n_m, h, d), want)
                 np.testing.assert_array_equal(c_oracle.unpack(packed, n_m, h, d), want)
+
+
+@pytest.mark.parametrize("n_m", [3, 5, 6, 7, 16])
+def test_wider_and_odd_mask_counts(n_m):
+    """Row f3 ("Scaling n_m to 16"): the layout and Eq. 3 for any n_m up to 16 -- the C
+    oracle's own unpacker and sum equal the numpy twin's explicit masked matrices, and the
+    all-zeros masks reduce to the plain projection n_m * g(0) * xW (sigmoid: n_m/2 * xW)."""
+    from oracle import ACT_SIGMOID, ACT_SWISH, COracle, mglu_forward_np, pack_np, unpack_np
+    rng = np.random.default_rng(n_m)
+    B, d, h = 2, 64, 9
+    x = rng.standard_normal((B, d))
+    Wt = rng.standard_normal((h, d))
+    bits = rng.integers(0, 2, (n_m, h, d)).astype(np.uint8)
+    o = COracle()
+    packed = o.pack(bits)
+    assert packed.size == h * d * n_m // 8
+    np.testing.assert_array_equal(packed, pack_np(bits))
+    np.testing.assert_array_equal(unpack_np(packed, n_m, h, d), bits)
+    y = o.forward(x, Wt, np.arange(h), packed, n_m, ACT_SWISH)
+    np.testing.assert_allclose(y, mglu_forward_np(x, Wt, bits, ACT_SWISH), rtol=1e-11, atol=1e-11)
+    zeros = o.pack(np.zeros_like(bits))
+    np.testing.assert_allclose(o.forward(x, Wt, np.arange(h), zeros, n_m, ACT_SIGMOID), n_m / 2 * x @ Wt.T,
+                               rtol=1e-12, atol=1e-12)
