@@ -98,7 +98,9 @@ typedef enum {
 
 /* Create a handle for one (d, h, n_m, act, dtype) layer on CUDA device `device`.
  *   d, h >= 1; d % 32 == 0 (the 32-column groups of the packed layout, reading R3);
- *   n_m in {1, 2, 4, 8}, or n_m = 0 for a DENSE projection out = x Wt^T (no masks, no activation;
+ *   n_m in {1, 2, 4, 8} (every kernel), or 3, 5, 6, 7, 16 (the SIMT kernel only: SURVEY row f3,
+ *   P:885-947; the packed layout is the same n_m words per 32-column group), or n_m = 0 for a
+ *   DENSE projection out = x Wt^T (no masks, no activation;
  *   `packed` may be NULL) -- the FFN down-projection W_o of SURVEY row f1 (bf16, MMA path,
  *   1 <= B <= 8, d % 128 == 0, x staged in shared memory: about 4 (B + 1) d bytes must fit next to
  *   two 32 KB stages; other configurations return UNSUPPORTED or CUDA from mglu_forward).

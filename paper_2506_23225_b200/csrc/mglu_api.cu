@@ -67,7 +67,10 @@ thread_local int t_routed_K = 0;   // K of the routed call (0: unknown -> every 
 const char* kStatusStr[] = {"MGLU_OK", "MGLU_ERR_INVALID_ARG", "MGLU_ERR_UNSUPPORTED",
                             "MGLU_ERR_MISALIGNED", "MGLU_ERR_CUDA", "MGLU_ERR_OOM"};
 
-bool valid_nm(int n_m) { return n_m == 1 || n_m == 2 || n_m == 4 || n_m == 8; }
+// mask counts: the tensor-core and HMMA kernels take n_m in {1, 2, 4, 8}; the SIMT kernel also
+// serves the other counts up to 8 and n_m = 16
+bool fast_nm(int n_m) { return n_m == 1 || n_m == 2 || n_m == 4 || n_m == 8; }
+bool valid_nm(int n_m) { return (n_m >= 1 && n_m <= 8) || n_m == 16; }
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 size_t elem_bytes(int dtype) { return dtype == MGLU_BF16 ? 2 : 4; }
 
@@ -136,7 +139,12 @@ cudaError_t simt_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const vo
   switch (hd->n_m) {
     case 1: return simt_act<T, PARTIALS, 1>(hd, x, B, Wt, codes, out, z, st);
     case 2: return simt_act<T, PARTIALS, 2>(hd, x, B, Wt, codes, out, z, st);
+    case 3: return simt_act<T, PARTIALS, 3>(hd, x, B, Wt, codes, out, z, st);
     case 4: return simt_act<T, PARTIALS, 4>(hd, x, B, Wt, codes, out, z, st);
+    case 5: return simt_act<T, PARTIALS, 5>(hd, x, B, Wt, codes, out, z, st);
+    case 6: return simt_act<T, PARTIALS, 6>(hd, x, B, Wt, codes, out, z, st);
+    case 7: return simt_act<T, PARTIALS, 7>(hd, x, B, Wt, codes, out, z, st);
+    case 16: return simt_act<T, PARTIALS, 16>(hd, x, B, Wt, codes, out, z, st);
     default: return simt_act<T, PARTIALS, 8>(hd, x, B, Wt, codes, out, z, st);
   }
 }
@@ -144,7 +152,8 @@ cudaError_t simt_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const vo
 // ------------------------------------------------------------------ MMA (TMA-fed decode) dispatch
 bool mma_can_serve(const mglu_ctx* hd, int64_t B) {
   // 128-column code blocks of 16 * n_m bytes tile the rows exactly
-  return hd->dtype == MGLU_BF16 && hd->d % 128 == 0 && B >= 1 && B <= 8 && hd->d <= 32768;
+  return hd->dtype == MGLU_BF16 && (hd->n_m == 0 || fast_nm(hd->n_m)) && hd->d % 128 == 0 && B >= 1 && B <= 8 &&
+         hd->d <= 32768;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -325,7 +334,8 @@ cudaError_t mma_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const voi
 // ------------------------------------------------------------------ tcgen05 (prefill) dispatch
 bool tc_can_serve(const mglu_ctx* hd, int64_t B) {
   // TMA of the mask words: rows of d/32 * n_m u32 words must be 16-byte multiples
-  return hd->dtype == MGLU_BF16 && hd->n_m > 0 && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 && B <= ((int64_t)1 << 31) - 1;
+  return hd->dtype == MGLU_BF16 && fast_nm(hd->n_m) && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 &&
+         B <= ((int64_t)1 << 31) - 1;
 }
 
 // 2-D row-major [rows][cols] bf16 tensor, box [brows][bcols]
@@ -451,7 +461,7 @@ constexpr int kAutoMmaMaxB = 4, kAutoSkMaxB = 24;
 
 bool sk_can_serve(const mglu_ctx* hd, int64_t B) {
   // 64-column units; mask-word rows of d/32 * n_m u32 words must be 16-byte multiples (TMA)
-  return hd->dtype == MGLU_BF16 && hd->n_m > 0 && hd->d % 64 == 0 && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 &&
+  return hd->dtype == MGLU_BF16 && fast_nm(hd->n_m) && hd->d % 64 == 0 && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 &&
          B <= kSkMaxB && (hd->n_m < 8 || B <= 32);
 }
 
@@ -459,12 +469,13 @@ bool sk_can_serve(const mglu_ctx* hd, int64_t B) {
 // path serves: G x (n_m + 1) x B x 128 fp32 partials and G flags (zeroed; owners re-arm them)
 cudaError_t sk_alloc(mglu_ctx* hd) {
   const size_t G = (size_t)hd->num_sms;
-  const size_t maxb = hd->n_m == 8 ? 32 : kSkMaxB;
+  const size_t maxb = !fast_nm(hd->n_m) ? 0 : hd->n_m == 8 ? 32 : kSkMaxB;   // (SIMT-only counts: no stream-K)
   cudaError_t e = cudaMalloc(&hd->sk_flags, G * sizeof(uint32_t));
   if (e != cudaSuccess) return e;
   e = cudaMemset(hd->sk_flags, 0, G * sizeof(uint32_t));
   if (e != cudaSuccess) return e;
   hd->sk_ws_bytes = G * (size_t)(hd->n_m + 1) * maxb * 128 * sizeof(float);
+  if (!hd->sk_ws_bytes) return cudaSuccess;
   e = cudaMalloc(&hd->sk_ws, hd->sk_ws_bytes);
   if (e != cudaSuccess) hd->sk_ws_bytes = 0;
   return e;
@@ -758,6 +769,7 @@ mglu_status mglu_router_topk(mglu_handle hd, const void* x, int64_t B, const voi
   if (B < 0 || !x || !Wr || !G) return set_err(hd, MGLU_ERR_INVALID_ARG, "null pointer or B < 0");
   if (K < 1 || K > hd->n_m) return set_err(hd, MGLU_ERR_INVALID_ARG, "K must be in [1, n_m]");
   if (hd->dtype != MGLU_BF16) return set_err(hd, MGLU_ERR_UNSUPPORTED, "router: bf16 handles only");
+  if (!fast_nm(hd->n_m)) return set_err(hd, MGLU_ERR_UNSUPPORTED, "router: n_m in {1, 2, 4, 8}");
   if (!aligned16(x) || !aligned16(Wr) || !aligned16(G)) return set_err(hd, MGLU_ERR_MISALIGNED, "16-byte alignment");
   hd->last_launches = 0;
   if (B == 0) return MGLU_OK;

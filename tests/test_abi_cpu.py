@@ -39,7 +39,10 @@ def test_status_strings_and_version(lib):
 def test_packed_bytes(lib):
     assert M.mglu_packed_mask_bytes(4096, 14336, 4) == 14336 * 4096 // 2
     assert M.mglu_packed_mask_bytes(64, 128, 1) == 64 * 128 // 8
-    assert M.mglu_packed_mask_bytes(64, 128, 3) == 0
+    assert M.mglu_packed_mask_bytes(64, 128, 3) == 64 * 128 * 3 // 8   # SIMT-only counts (row f3)
+    assert M.mglu_packed_mask_bytes(64, 128, 16) == 64 * 128 * 2
+    assert M.mglu_packed_mask_bytes(64, 128, 9) == 0
+    assert M.mglu_packed_mask_bytes(64, 128, 0) == 0
     assert M.mglu_packed_mask_bytes(48, 128, 4) == 0         # d % 32 != 0
     assert M.mglu_packed_mask_bytes(-1, 128, 1) == 0
 
@@ -49,7 +52,8 @@ def test_create_argument_errors(lib):
     assert lib.mglu_create(None, 64, 128, 1, 1, 0, 0) == M.MGLU_ERR_INVALID_ARG
     assert lib.mglu_create(ctypes.byref(hd), 0, 128, 1, 1, 0, 0) == M.MGLU_ERR_INVALID_ARG
     assert lib.mglu_create(ctypes.byref(hd), 64, 128, 1, 9, 0, 0) == M.MGLU_ERR_INVALID_ARG
-    assert lib.mglu_create(ctypes.byref(hd), 64, 128, 3, 1, 0, 0) == M.MGLU_ERR_UNSUPPORTED
+    assert lib.mglu_create(ctypes.byref(hd), 64, 128, 9, 1, 0, 0) == M.MGLU_ERR_UNSUPPORTED
+    assert lib.mglu_create(ctypes.byref(hd), 64, 128, 17, 1, 0, 0) == M.MGLU_ERR_UNSUPPORTED
     assert lib.mglu_create(ctypes.byref(hd), 60, 128, 1, 1, 0, 0) == M.MGLU_ERR_UNSUPPORTED
     assert lib.mglu_destroy(None) == M.MGLU_OK
     assert lib.mglu_forward(None, None, 1, None, None, None, None) == M.MGLU_ERR_INVALID_ARG
@@ -95,11 +99,20 @@ def test_host_pack_rejects_non_binary(lib):
         M.mglu_pack_masks_host(bits)
     assert e.value.status == M.MGLU_ERR_INVALID_ARG
     with pytest.raises(M.MgluError) as e:
-        M.mglu_pack_masks_host(np.zeros((3, 4, 32), dtype=np.uint8))
+        M.mglu_pack_masks_host(np.zeros((9, 4, 32), dtype=np.uint8))   # n_m in 1..8 or 16 (row f3)
     assert e.value.status == M.MGLU_ERR_UNSUPPORTED
     with pytest.raises(M.MgluError) as e:                   # d % 32 != 0 (layout groups, R3)
         M.mglu_pack_masks_host(np.zeros((2, 4, 48), dtype=np.uint8))
     assert e.value.status == M.MGLU_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("n_m", [3, 5, 6, 7, 16])
+def test_host_pack_wide_counts_match_oracle(lib, n_m):
+    """The library's host packer equals the oracle's for the SIMT-only mask counts (row f3)."""
+    from oracle import pack_np
+    bits = np.random.default_rng(n_m).integers(0, 2, (n_m, 5, 64)).astype(np.uint8)
+    np.testing.assert_array_equal(M.mglu_pack_masks_host(bits), pack_np(bits))
+    np.testing.assert_array_equal(M.mglu_unpack_masks_host(pack_np(bits), n_m, 5, 64), bits)
 
 
 def test_product_package_does_not_import_oracle():
