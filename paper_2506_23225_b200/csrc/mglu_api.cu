@@ -24,6 +24,10 @@
 #include "pack.cuh"
 #include "router.cuh"
 
+#ifndef MGLU_DEC_SMEM_KB
+#define MGLU_DEC_SMEM_KB 200   // shared-memory budget of the HMMA decode kernel (ring depth)
+#endif
+
 struct mglu_ctx {
   int64_t d = 0, h = 0;
   int n_m = 0, act = 0, dtype = 0, device = 0;
@@ -272,7 +276,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   const size_t partbytes = (size_t)mglu::kDecConsumers * 32 * NB * ((KSEL > 0 ? KSEL : NM) + 1) * 4;
   const size_t fixed = xbytes + partbytes + 1024;
   // (dense handles with a long reduction stage a large x: let them use the whole opt-in budget)
-  const size_t cap = std::min<size_t>((size_t)hd->max_smem_optin, NM == 0 ? (size_t)hd->max_smem_optin : 200 * 1024);
+  const size_t cap = std::min<size_t>((size_t)hd->max_smem_optin, NM == 0 ? (size_t)hd->max_smem_optin : (size_t)MGLU_DEC_SMEM_KB * 1024);
   if (cap < fixed) return cudaErrorInvalidConfiguration;
   int S = (int)((cap - fixed) / (SB + 16));
   S = std::min(8, S);
