@@ -5,7 +5,8 @@ Default workload (N=1): BASELINE.json's target row -- batch-1 SwiMGLU, n_m = 4, 
 h = 14336, bf16 (config 3 at B = 1).  One step = one forward call (all SURVEY 8(a) rows run in
 one kernel).  For N > 1 the layer's output columns (h) are column-sharded across ranks with no
 data-path collective (reading R-e); value = the whole layer's algorithmic bytes / max-over-ranks
-time, "scaling": "strong" (total work fixed).
+time.  Default "scaling": "weak" -- the layer is N column blocks wide and every GPU owns one block of
+the N=1 width (per-GPU work fixed); --scaling strong splits the N=1 layer instead.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mglu|reference] [--workload NAME]
 
@@ -281,6 +282,7 @@ def run_reference(args, ws, rank):
         return None
     from oracle import ACT_NAMES, COracle
     d, h, n_m, B, act, desc = WORKLOADS[args.workload]
+    h = h * ws if (ws > 1 and args.scaling == "weak") else h     # the mglu arm's layer at this N
     o = COracle()
     # torchrun sets OMP_NUM_THREADS=1 per process; rank 0 is the only rank working here, so the
     # oracle gets the host's cores (its result does not depend on the thread count)
@@ -322,7 +324,10 @@ def run_mglu(args, ws, rank, local):
     from paper_2506_23225_b200.shard import shard_bounds
     d, h, n_m, B, act, desc = WORKLOADS[args.workload]
     # column shard of h (no exchange on the hot path): this rank's rows of Wt and of the codes
-    lo, hi = shard_bounds(h, ws, rank)
+    # weak scaling (default): the layer is N column blocks wide, each rank owns one block of the N=1
+    # workload's width (per-GPU work fixed); strong: the N=1 layer itself is split across the ranks
+    h_total = h * ws if args.scaling == "weak" else h
+    lo, hi = shard_bounds(h_total, ws, rank)
     h_loc = hi - lo
     L = args.layers
     x, layers = make_layers(d, h_loc, n_m, B, L, seed=0, rank=rank)
@@ -393,11 +398,11 @@ def run_mglu(args, ws, rank, local):
         barrier(ws)
         sampler.stop()
     el_max = max_over_ranks(ws, el)
-    units_layer, scale, unit, metric = work(d, h, n_m, B)
+    units_layer, scale, unit, metric = work(d, h_total, n_m, B)
     units_rank = work(d, h_loc, n_m, B)[0]
     bytes_rank = algorithmic_bytes(d, h_loc, n_m, B)
     if args.ffn:                                              # + the dense W_o pass (x = y, out = [B][d])
-        units_layer += algorithmic_bytes(h, d, 0, B)
+        units_layer += algorithmic_bytes(h_total, d, 0, B)
         units_rank += algorithmic_bytes(h_loc, d, 0, B)
         bytes_rank += algorithmic_bytes(h_loc, d, 0, B)
         metric = "SwiMGLU FFN block (up-proj + W_o) HBM GB/s at batch B (algorithmic bytes of both layers / time per step)"
@@ -453,7 +458,7 @@ def run_mglu(args, ws, rank, local):
         barrier(ws)
         el_e2e = max_over_ranks(ws, el_e2e)
         e2e = {"value": units_layer * args.steps / el_e2e / scale, "unit": unit,
-               "h2d_bytes_per_step": B * d * 2 * ws, "d2h_bytes_per_step": B * h * 2,
+               "h2d_bytes_per_step": B * d * 2 * ws, "d2h_bytes_per_step": B * h_total * 2,
                "us_per_call": el_e2e / args.steps * 1e6, "streams": E,
                "how": "mglu_forward_host per step (pinned x -> device, forward, y -> pinned host), steps "
                       f"alternating over {E} streams/handles so copies overlap kernels"}
@@ -472,10 +477,11 @@ def run_mglu(args, ws, rank, local):
         out = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": el_max / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "scaling": args.scaling if ws > 1 else "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (device-drawn, seeded: x~N(0,1), Wt~U(+-1/sqrt(d)), codes i.i.d. Bernoulli(0.5) bits)",
-            "config": {"workload": desc, "d": d, "h": h, "n_m": n_m, "batch": B, "act": act,
-                       "parallelism": f"column-shard h/{ws}" if ws > 1 else "single GPU",
+            "config": {"workload": desc, "d": d, "h": h, "h_total": h_total, "n_m": n_m, "batch": B, "act": act,
+                       "parallelism": (f"column-shard of a {h_total}-wide layer over {ws} GPUs, {hi - lo} columns each "
+                                       f"({args.scaling} scaling)") if ws > 1 else "single GPU",
                        "l2": f"inputs larger than L2: {L} distinct layer copies ({L * bytes_rank / 1e6:.0f} MB/rank) rotated, no flush",
                        "kernel_path": path_used, "launch": "PDL (programmatic dependent launch) per call",
                        **({"topk": args.topk, "step": "router_topk + forward_routed (2 launches)"} if args.topk else {}),
@@ -516,6 +522,8 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--e2e-streams", type=int, default=3, help="streams the e2e (host-buffer) leg alternates over")
     ap.add_argument("--topk", type=int, default=0, help="Top-K routed MGLU: K kept masks (router + routed forward)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N>1: weak = each GPU a full-width column block (work per GPU fixed); strong = split the N=1 layer")
     ap.add_argument("--ffn", action="store_true", help="FFN block: up-projection + dense W_o (+ all-reduce under torchrun)")
     ap.add_argument("--no-comparator", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
