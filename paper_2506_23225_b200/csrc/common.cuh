@@ -14,46 +14,64 @@ enum Act : int { kIdentity = 0, kSwish = 1, kGelu = 2, kRelu = 3, kSigmoid = 4 }
 
 // g of Eq. 1/3 in fp32 (reading R5).  expf/erff (not the __ intrinsics): the epilogue is a
 // negligible share of the decode call and the f32 path is held to 1e-5 normwise.
+// kRuntimeAct: one instantiation serves every g, chosen by a runtime code (the epilogue is a
+// negligible share of every regime, so only the default Swish gets its own compile-time copy)
+constexpr int kRuntimeAct = 5;
+
+__device__ __forceinline__ float act_rt(int act, float z);
+
 template <int ACT>
-__device__ __forceinline__ float act_g(float z) {
-  if constexpr (ACT == kIdentity) return z;
+__device__ __forceinline__ float act_g(float z, int act = 0) {
+  if constexpr (ACT == kRuntimeAct) return act_rt(act, z);
+  else if constexpr (ACT == kIdentity) return z;
   else if constexpr (ACT == kSwish) return z / (1.0f + expf(-z));
   else if constexpr (ACT == kGelu) return 0.5f * z * (1.0f + erff(z * 0.70710678118654752f));
   else if constexpr (ACT == kRelu) return fmaxf(z, 0.0f);
   else return 1.0f / (1.0f + expf(-z));
 }
 
+__device__ __forceinline__ float act_rt(int act, float z) {
+  switch (act) {
+    case kIdentity: return act_g<kIdentity>(z);
+    case kSwish: return act_g<kSwish>(z);
+    case kGelu: return act_g<kGelu>(z);
+    case kRelu: return act_g<kRelu>(z);
+    default: return act_g<kSigmoid>(z);
+  }
+}
+
 // Eq. 3 epilogue for one output: y = sum_i g(s_i) * (t - s_i)  (value = t - s_i)
 template <int ACT, int NM>
-__device__ __forceinline__ float mglu_epilogue(float t, const float (&s)[NM]) {
+__device__ __forceinline__ float mglu_epilogue(float t, const float (&s)[NM], int act = 0) {
   float y = 0.0f;
 #pragma unroll
-  for (int i = 0; i < NM; ++i) y = fmaf(act_g<ACT>(s[i]), t - s[i], y);
+  for (int i = 0; i < NM; ++i) y = fmaf(act_g<ACT>(s[i], act), t - s[i], y);
   return y;
 }
 
 // Top-K routed epilogue (Appendix B): y = sum_i G_i g(s_i) (t - s_i); gw == nullptr is
 // the plain Eq. 3 (every G_i = 1)
 template <int ACT, int NM>
-__device__ __forceinline__ float mglu_epilogue_w(float t, const float (&s)[NM], const float* gw) {
-  if (!gw) return mglu_epilogue<ACT, NM>(t, s);
+__device__ __forceinline__ float mglu_epilogue_w(float t, const float (&s)[NM], const float* gw, int act = 0) {
+  if (!gw) return mglu_epilogue<ACT, NM>(t, s, act);
   float y = 0.0f;
 #pragma unroll
-  for (int i = 0; i < NM; ++i) y = fmaf(gw[i] * act_g<ACT>(s[i]), t - s[i], y);
+  for (int i = 0; i < NM; ++i) y = fmaf(gw[i] * act_g<ACT>(s[i], act), t - s[i], y);
   return y;
 }
 
 // Partial-mask ablation variants (reading R20: per mask term): 1 NG gate = t,
 // 2 NV value = t, 3 NM both; 0 = Eq. 3.  Optional routed weights gw.
 template <int ACT, int NM>
-__device__ __forceinline__ float mglu_epilogue_v(float t, const float (&s)[NM], const float* gw, int variant) {
-  if (variant == 0) return mglu_epilogue_w<ACT, NM>(t, s, gw);
+__device__ __forceinline__ float mglu_epilogue_v(float t, const float (&s)[NM], const float* gw, int variant,
+                                                 int act = 0) {
+  if (variant == 0) return mglu_epilogue_w<ACT, NM>(t, s, gw, act);
   float y = 0.0f;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
     const float gate = (variant & 1) ? t : s[i];
     const float value = (variant & 2) ? t : t - s[i];
-    y = fmaf((gw ? gw[i] : 1.0f) * act_g<ACT>(gate), value, y);
+    y = fmaf((gw ? gw[i] : 1.0f) * act_g<ACT>(gate, act), value, y);
   }
   return y;
 }

@@ -78,6 +78,7 @@ struct TcParams {
   __nv_bfloat16* out;        // [B][h]
   const float* G;            // Top-K routed gate weights [B][n_m] (nullptr: every weight 1)
   int variant;               // partial-mask ablation variant (0 = Eq. 3)
+  int act;                   // g when the kernel is the kRuntimeAct instantiation
   int B, d, h;
   int stages;
 };
@@ -276,7 +277,7 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
           const float gate = (p.variant & 1) ? t : sg;                    // ablation variants
           const float value = (p.variant & 2) ? t : t - sg;
           const float wgt = p.G ? (tq < p.B ? p.G[(size_t)tq * NM + moff + i] : 0.f) : 1.f;   // routed (App. B)
-          acc = fmaf(wgt * act_g<ACT>(gate), value, acc);                 // g(s_i) (t - s_i)
+          acc = fmaf(wgt * act_g<ACT>(gate, p.act), value, acc);                 // g(s_i) (t - s_i)
         }
         yp[ch][q] = acc;
       }

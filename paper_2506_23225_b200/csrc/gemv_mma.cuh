@@ -58,6 +58,7 @@ struct DecParams {
   __nv_bfloat16* out;
   const float* G;            // Top-K routed gate weights [B][n_m] (nullptr: plain Eq. 3)
   int variant;               // partial-mask ablation variant (0 = Eq. 3; 1 NG, 2 NV, 3 NM)
+  int act;                   // g when the kernel is the kRuntimeAct instantiation
   int B, d, h;
   int rows_base, rows_rem;   // CTA c owns rows_base + (c < rows_rem) rows
   int stages;                // ring depth
@@ -327,9 +328,9 @@ gemv_mma_kernel(const DecParams p,
             const float* gw = p.G + (size_t)tok * NM;
 #pragma unroll
             for (int k = 0; k < KSEL; ++k)
-              if ((valid >> k) & 1u) y = fmaf(gw[sel[k]] * act_g<ACT>(sv[k]), v[nb][0] - sv[k], y);
+              if ((valid >> k) & 1u) y = fmaf(gw[sel[k]] * act_g<ACT>(sv[k], p.act), v[nb][0] - sv[k], y);
           } else {
-            y = mglu_epilogue_v<ACT, NM>(v[nb][0], sv, p.G ? p.G + (size_t)tok * NM : nullptr, p.variant);   // Eq. 3 / routed / variant
+            y = mglu_epilogue_v<ACT, NM>(v[nb][0], sv, p.G ? p.G + (size_t)tok * NM : nullptr, p.variant, p.act);   // Eq. 3 / routed / variant
           }
           p.out[(size_t)tok * p.h + r0 + row] = __float2bfloat16_rn(y);
         }

@@ -54,7 +54,7 @@ template <typename T, int NM, int ACT, bool PARTIALS>
 __global__ void __launch_bounds__(256)
 gemv_simt_kernel(const T* __restrict__ x, int B, int d, const T* __restrict__ Wt,
                  const uint8_t* __restrict__ codes, int h, T* __restrict__ out,
-                 float* __restrict__ z, const float* __restrict__ G, int variant) {
+                 float* __restrict__ z, const float* __restrict__ G, int variant, int act) {
   pdl_wait();
   const int lane = threadIdx.x & 31;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
@@ -117,7 +117,7 @@ gemv_simt_kernel(const T* __restrict__ x, int B, int d, const T* __restrict__ Wt
               }
             } else {
               IoT<T>::store(out + (size_t)(b0 + b) * h + j,
-                            mglu_epilogue_v<ACT, NM>(t[b], s[b], G ? G + (size_t)(b0 + b) * NM : nullptr, variant));
+                            mglu_epilogue_v<ACT, NM>(t[b], s[b], G ? G + (size_t)(b0 + b) * NM : nullptr, variant, act));
             }
           }
         }

@@ -74,15 +74,6 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ float act_rt(int act, float z) {
-  switch (act) {
-    case kIdentity: return act_g<kIdentity>(z);
-    case kSwish: return act_g<kSwish>(z);
-    case kGelu: return act_g<kGelu>(z);
-    case kRelu: return act_g<kRelu>(z);
-    default: return act_g<kSigmoid>(z);
-  }
-}
 
 // geometry of one instantiation: NM masks, BN token columns, MG masker groups of 4 warps
 template <int NM, int BN, int MG> struct SkCfg {

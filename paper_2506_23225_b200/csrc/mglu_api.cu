@@ -122,18 +122,15 @@ cudaError_t run_simt(mglu_ctx* hd, const void* x, int B, const void* Wt, const v
   if (blocks > cap) blocks = cap;
   return launch_pdl(mglu::gemv_simt_kernel<T, NM, ACT, PARTIALS>, dim3((unsigned)blocks),
                     dim3(warps_per_block * 32), 0, st, (const T*)x, B, (int)hd->d, (const T*)Wt,
-                    (const uint8_t*)codes, (int)hd->h, (T*)out, z, t_routed_G, hd->variant);
+                    (const uint8_t*)codes, (int)hd->h, (T*)out, z, t_routed_G, hd->variant, hd->act);
 }
 
 template <typename T, bool PARTIALS, int NM>
 cudaError_t simt_act(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
                      void* out, float* z, cudaStream_t st) {
   switch (hd->act) {
-    case MGLU_ACT_IDENTITY: return run_simt<T, NM, mglu::kIdentity, PARTIALS>(hd, x, B, Wt, codes, out, z, st);
     case MGLU_ACT_SWISH: return run_simt<T, NM, mglu::kSwish, PARTIALS>(hd, x, B, Wt, codes, out, z, st);
-    case MGLU_ACT_GELU: return run_simt<T, NM, mglu::kGelu, PARTIALS>(hd, x, B, Wt, codes, out, z, st);
-    case MGLU_ACT_RELU: return run_simt<T, NM, mglu::kRelu, PARTIALS>(hd, x, B, Wt, codes, out, z, st);
-    default: return run_simt<T, NM, mglu::kSigmoid, PARTIALS>(hd, x, B, Wt, codes, out, z, st);
+    default: return run_simt<T, NM, mglu::kRuntimeAct, PARTIALS>(hd, x, B, Wt, codes, out, z, st);   // g at runtime
   }
 }
 
@@ -251,6 +248,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   p.out = (__nv_bfloat16*)out;
   p.G = t_routed_G;
   p.variant = hd->variant;
+  p.act = hd->act;
   p.B = B;
   p.d = (int)hd->d;
   p.h = (int)hd->h;
@@ -316,11 +314,8 @@ template <int NM>
 cudaError_t mma_act(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes, void* out,
                     cudaStream_t st) {
   switch (hd->act) {
-    case MGLU_ACT_IDENTITY: return run_mma<NM, mglu::kIdentity>(hd, x, B, Wt, codes, out, st);
     case MGLU_ACT_SWISH: return run_mma<NM, mglu::kSwish>(hd, x, B, Wt, codes, out, st);
-    case MGLU_ACT_GELU: return run_mma<NM, mglu::kGelu>(hd, x, B, Wt, codes, out, st);
-    case MGLU_ACT_RELU: return run_mma<NM, mglu::kRelu>(hd, x, B, Wt, codes, out, st);
-    default: return run_mma<NM, mglu::kSigmoid>(hd, x, B, Wt, codes, out, st);
+    default: return run_mma<NM, mglu::kRuntimeAct>(hd, x, B, Wt, codes, out, st);   // g at runtime
   }
 }
 
@@ -394,6 +389,7 @@ cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   p.out = (__nv_bfloat16*)out;
   p.G = t_routed_G;
   p.variant = hd->variant;
+  p.act = hd->act;
   p.B = (int)B;
   p.d = (int)hd->d;
   p.h = (int)hd->h;
@@ -441,11 +437,8 @@ template <int NM>
 cudaError_t tc_act(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
                    cudaStream_t st) {
   switch (hd->act) {
-    case MGLU_ACT_IDENTITY: return run_tc<NM, mglu::kIdentity>(hd, x, B, Wt, codes, out, st);
     case MGLU_ACT_SWISH: return run_tc<NM, mglu::kSwish>(hd, x, B, Wt, codes, out, st);
-    case MGLU_ACT_GELU: return run_tc<NM, mglu::kGelu>(hd, x, B, Wt, codes, out, st);
-    case MGLU_ACT_RELU: return run_tc<NM, mglu::kRelu>(hd, x, B, Wt, codes, out, st);
-    default: return run_tc<NM, mglu::kSigmoid>(hd, x, B, Wt, codes, out, st);
+    default: return run_tc<NM, mglu::kRuntimeAct>(hd, x, B, Wt, codes, out, st);   // g at runtime
   }
 }
 
