@@ -48,6 +48,9 @@ namespace mglu {
 // 128 / 16, for ring depth and TMEM room)
 template <int NM> __host__ __device__ constexpr int sk_ks() { return NM == 8 ? 128 : 256; }
 template <int NM> __host__ __device__ constexpr int sk_ka() { return NM == 8 ? 16 : 64; }
+#ifndef MGLU_SK_SS_T
+#define MGLU_SK_SS_T 0   // 1: t's MMA reads W from shared memory (SS); TMEM slots hold the masked copies only
+#endif
 
 struct SkParams {
   __nv_bfloat16* out;   // [B][h]
@@ -80,7 +83,8 @@ template <int NM, int BN, int MG> struct SkCfg {
   static constexpr int NOP = NM + 1;
   static constexpr int KS = sk_ks<NM>();
   static constexpr int KA = sk_ka<NM>();
-  static constexpr int SLOT = NOP * KA / 2;
+  static constexpr int TOP = MGLU_SK_SS_T ? 0 : 1;   // W copies in a TMEM slot
+  static constexpr int SLOT = (NM + TOP) * KA / 2;
   static constexpr int ACC = NOP * BN;
   static constexpr int NACC = 2 * ACC + 2 * MG * SLOT <= 512 ? 2 : 1;
   static constexpr int SA_FIT = (512 - NACC * ACC) / SLOT / MG * MG;
@@ -197,9 +201,13 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
             const uint64_t bdesc = smem_desc_kmajor(st + WB + (k16 >> 2) * BN * 128, 128) + (uint64_t)((k16 & 3) * 2);
             const uint32_t accum = (seg_first && k16 == 0) ? 0u : 1u;
             const uint32_t asl = tmem + A_COL0 + (uint32_t)(sa * SLOT + kk * 8);
+            if constexpr (C::TOP == 0) {
+              const uint64_t adesc = smem_desc_kmajor(st + (k16 >> 2) * 16384, 128) + (uint64_t)((k16 & 3) * 2);
+              tc_mma_ss(dacc, adesc, bdesc, IDESC, accum);
+            }
 #pragma unroll
-            for (int o = 0; o < NOP; ++o)
-              tc_mma_ts(dacc + (uint32_t)(o * BN), asl + (uint32_t)(o * WW), bdesc, IDESC, accum);
+            for (int o = 1 - C::TOP; o < NOP; ++o)
+              tc_mma_ts(dacc + (uint32_t)(o * BN), asl + (uint32_t)((o - 1 + C::TOP) * WW), bdesc, IDESC, accum);
           }
           tc_commit(&a_empty[sa]);
           if (a == APS - 1) tc_commit(&empty[s]);
@@ -243,14 +251,14 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
         mbar_wait(&a_empty[sa], ((uint32_t)(js / SA) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t a0 = a_lane + (uint32_t)(sa * SLOT);
-        tmem_st_n<WW>(a0, w);
+        if constexpr (C::TOP) tmem_st_n<WW>(a0, w);
 #pragma unroll
         for (int i = 0; i < NM; ++i) {
           uint32_t op[WW];
 #pragma unroll
           for (int q = 0; q < WW; ++q)                     // pair q: group q / PPG, bits (p, p + 16)
             op[q] = sign_flip(w[q], cw[q / PPG][i], 1u << (15 - pair0 - (q % PPG)));
-          tmem_st_n<WW>(a0 + (uint32_t)((1 + i) * WW), op);
+          tmem_st_n<WW>(a0 + (uint32_t)((C::TOP + i) * WW), op);
         }
         tmem_st_wait();
         tc_fence_before();
