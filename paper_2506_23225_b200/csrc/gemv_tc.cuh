@@ -48,6 +48,9 @@ namespace mglu {
 // 128 / 16, for ring depth and TMEM room)
 template <int NM> __host__ __device__ constexpr int sk_ks() { return NM == 8 ? 128 : 256; }
 template <int NM> __host__ __device__ constexpr int sk_ka() { return NM == 8 ? 16 : 64; }
+#ifndef MGLU_SK_EPI_CH
+#define MGLU_SK_EPI_CH 4 // epilogue tokens per chunk (8 and 16 measured slower, profiles/r01_tcdec_experiments.txt §11)
+#endif
 #ifndef MGLU_SK_SS_T
 #define MGLU_SK_SS_T 0   // 1: t's MMA reads W from shared memory (SS); TMEM slots hold the masked copies only
 #endif
@@ -272,7 +275,8 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
     const int m = quarter * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     const int B = p.B;
-    constexpr int CH = 4;
+    constexpr int CH = MGLU_SK_EPI_CH;                 // tokens per epilogue chunk (multiple of 4)
+    static_assert(CH % 4 == 0 && BN % CH == 0, "epilogue chunk");
     const int nch = (B + CH - 1) / CH;
     pdl_wait();
     int set = 0;
@@ -301,13 +305,18 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
       }
       for (int ch = 0; ch < nch; ++ch) {
         float f[NOP][CH];
+        {
+          uint32_t v[NOP][CH];                         // all loads of the chunk in flight, one wait
 #pragma unroll
-        for (int o = 0; o < NOP; ++o) {
-          uint32_t v[CH];
-          tmem_ld4(abase + (uint32_t)(o * BN + ch * CH), v);
+          for (int o = 0; o < NOP; ++o)
+#pragma unroll
+            for (int c4 = 0; c4 < CH / 4; ++c4)
+              tmem_ld4(abase + (uint32_t)(o * BN + ch * CH + c4 * 4), *reinterpret_cast<uint32_t(*)[4]>(&v[o][c4 * 4]));
           tmem_ld_wait();
 #pragma unroll
-          for (int q = 0; q < CH; ++q) f[o][q] = __uint_as_float(v[q]);
+          for (int o = 0; o < NOP; ++o)
+#pragma unroll
+            for (int q = 0; q < CH; ++q) f[o][q] = __uint_as_float(v[o][q]);
         }
         if (!owner) {
           float* wsp = p.ws + (size_t)cta * NOP * B * 128 + m;
