@@ -5,4 +5,5 @@ ncu -i gpurun_out/prof_$tag.ncu-rep --page raw --csv > gpurun_out/prof_${tag}_ra
 ncu -i gpurun_out/prof_$tag.ncu-rep --page details --csv > gpurun_out/prof_${tag}_details.csv 2>/dev/null
 ncu -i gpurun_out/prof_$tag.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_${tag}_source.csv 2>/dev/null
 python3 tools/ncu_summary.py gpurun_out/prof_${tag}_raw.csv gpurun_out/prof_${tag}_details.csv > gpurun_out/prof_${tag}_summary.txt 2>&1
+[ -z "$KEEP_REP" ] && rm -f gpurun_out/prof_$tag.ncu-rep   # gpurun brings back <= 64 MiB
 echo "== $tag"; cat gpurun_out/prof_${tag}_summary.txt
