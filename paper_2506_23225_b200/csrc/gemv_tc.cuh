@@ -51,6 +51,9 @@ template <int NM> __host__ __device__ constexpr int sk_ka() { return NM == 8 ? 1
 #ifndef MGLU_SK_EPI_CH
 #define MGLU_SK_EPI_CH 4 // epilogue tokens per chunk (8 and 16 measured slower, profiles/r01_tcdec_experiments.txt §11)
 #endif
+#ifndef MGLU_SK_NOFIXUP
+#define MGLU_SK_NOFIXUP 0  // timing ablation only (wrong results): no partial stores / owner fix-up
+#endif
 #ifndef MGLU_SK_SS_T
 #define MGLU_SK_SS_T 0   // 1: t's MMA reads W from shared memory (SS); TMEM slots hold the masked copies only
 #endif
@@ -293,7 +296,7 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
       const uint32_t abase = lane_base + (uint32_t)(set * ACC);
       const int grow = tile * 128 + m;
       int ncon = 0;
-      if (owner && !whole) {
+      if (owner && !whole && !MGLU_SK_NOFIXUP) {
         while (cta + 1 + ncon < (int)gridDim.x && sk_unit0(p, cta + 1 + ncon) < tile_end) ++ncon;
         for (int k = 1; k <= ncon; ++k) {
           uint32_t polls = 0;
@@ -319,6 +322,7 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
             for (int q = 0; q < CH; ++q) f[o][q] = __uint_as_float(v[o][q]);
         }
         if (!owner) {
+          if (MGLU_SK_NOFIXUP) continue;
           float* wsp = p.ws + (size_t)cta * NOP * B * 128 + m;
 #pragma unroll
           for (int o = 0; o < NOP; ++o)
