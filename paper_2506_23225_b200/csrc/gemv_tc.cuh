@@ -54,6 +54,9 @@ template <int NM> __host__ __device__ constexpr int sk_ka() { return NM == 8 ? 1
 #ifndef MGLU_SK_NOFIXUP
 #define MGLU_SK_NOFIXUP 0  // timing ablation only (wrong results): no partial stores / owner fix-up
 #endif
+#ifndef MGLU_SK_ACC2_SLOTS
+#define MGLU_SK_ACC2_SLOTS 2  // A slots per masker group that must fit beside two accumulator sets
+#endif
 #ifndef MGLU_SK_SS_T
 #define MGLU_SK_SS_T 0   // 1: t's MMA reads W from shared memory (SS); TMEM slots hold the masked copies only
 #endif
@@ -92,7 +95,7 @@ template <int NM, int BN, int MG> struct SkCfg {
   static constexpr int TOP = MGLU_SK_SS_T ? 0 : 1;   // W copies in a TMEM slot
   static constexpr int SLOT = (NM + TOP) * KA / 2;
   static constexpr int ACC = NOP * BN;
-  static constexpr int NACC = 2 * ACC + 2 * MG * SLOT <= 512 ? 2 : 1;
+  static constexpr int NACC = 2 * ACC + MGLU_SK_ACC2_SLOTS * MG * SLOT <= 512 ? 2 : 1;
   static constexpr int SA_FIT = (512 - NACC * ACC) / SLOT / MG * MG;
   static constexpr int SA = SA_FIT > 4 * MG ? 4 * MG : SA_FIT;
   static constexpr int WPS = KS / 32 * NM;
