@@ -5,13 +5,16 @@ Default workload (N=1): BASELINE.json's target row -- batch-1 SwiMGLU, n_m = 4, 
 h = 14336, bf16 (config 3 at B = 1).  One step = one forward call (all SURVEY 8(a) rows run in
 one kernel).  For N > 1 the layer's output columns (h) are column-sharded across ranks with no
 data-path collective (reading R-e); value = the whole layer's algorithmic bytes / max-over-ranks
-time.  Default "scaling": "weak" -- the layer is N column blocks wide and every GPU owns one block of
-the N=1 width (per-GPU work fixed); --scaling strong splits the N=1 layer instead.
+time.  Default "scaling": "strong" -- the BASELINE layer itself is split across the N ranks (each owns
+h/N output columns); --scaling weak makes the layer N column blocks wide (per-GPU work fixed).
+After timing, N>1 runs all-gather the h-sliced outputs over NCCL (the full-output check) and rank 0
+compares them with the unsharded layer computed on its own GPU: bit-identical by construction.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mglu|reference] [--workload NAME]
 
-Timing: W untimed warm-up steps, a ~0.3 s clock window (untimed, nvidia-smi/NVML sampled), then
-EXACTLY K steps between CUDA events on the launching stream, bracketed by barrier + synchronize.
+Timing: W untimed warm-up steps, then EXACTLY K steps between CUDA events on the launching stream,
+bracketed by barrier + synchronize, behind an untimed device-side spin that lets the host enqueue
+them ahead; NVML samples SM clocks and throttle reasons during the spin and the timed region.
 L2: the per-step inputs are larger than L2 -- L distinct copies of the layer (W + codes,
 L x 147 MB) are rotated, so every step streams cold weights (no flush kernel is needed).
 """
@@ -92,7 +95,7 @@ class ClockSampler:
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
 
     def __init__(self, device_index: int, period_s: float = 0.005):
-        self.samples, self.reasons, self.ok = [], set(), False
+        self.samples, self.power, self.reasons, self.ok = [], [], set(), False
         self.period = period_s
         try:
             import pynvml
@@ -112,6 +115,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit:
@@ -135,7 +139,8 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
         med = statistics.median(self.samples) if self.samples else None
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+                "samples": len(self.samples),
+                "power_w_max": max(self.power) if self.power else None}
 
 
 # ---------------------------------------------------------------- distributed plumbing
@@ -173,29 +178,72 @@ def max_over_ranks(ws, value: float) -> float:
 
 
 # ---------------------------------------------------------------- inputs (synthetic, seeded)
-def make_layers(d, h_local, n_m, B, L, seed, rank):
-    """L distinct copies of the rank's layer shard, drawn on the device (synth recipe: x ~ N(0,1),
-    Wt ~ U(+-1/sqrt(d)), code bits i.i.d. Bernoulli(0.5))."""
+def make_layers(d, h_total, n_m, B, L, seed, lo, hi):
+    """L distinct copies of the whole layer, drawn on the device from the seed alone (synth recipe:
+    x ~ N(0,1), Wt ~ U(+-1/sqrt(d)), code bits i.i.d. Bernoulli(0.5)), and this rank's rows
+    [lo, hi) of each as views (a column shard of Wt and of the packed codes is a pointer offset)."""
     from synth import random_packed_codes
-    g = torch.Generator(device="cuda").manual_seed(seed * 1000 + rank)
+    g = torch.Generator(device="cuda").manual_seed(seed * 1000)
     x = torch.randn(B, d, device="cuda", generator=g).to(torch.bfloat16)
-    layers = []
+    rb = d * n_m // 8
+    fulls, shards = [], []
     for li in range(L):
-        Wt = ((torch.rand(h_local, d, device="cuda", generator=g) * 2 - 1) / d ** 0.5).to(torch.bfloat16)
-        codes = random_packed_codes(seed * 7919 + rank * 97 + li, h_local, d, n_m, device="cuda")
-        layers.append((Wt, codes))
-    return x, layers
+        Wt = ((torch.rand(h_total, d, device="cuda", generator=g) * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+        codes = random_packed_codes(seed * 7919 + li, h_total, d, n_m, device="cuda")
+        fulls.append((Wt, codes))
+        shards.append((Wt[lo:hi], codes[lo * rb:hi * rb]))
+    return x, fulls, shards
+
+
+def enqueue_ahead(stream, K, us_per_step=None):
+    """A device-side spin (untimed, before the start event) so the host enqueues the timed launches
+    while the GPU is busy: the timed region then sees back-to-back launches, not host gaps (the
+    first launch's latency, a slow ctypes call, or the NVML clock sampler briefly stalling the
+    launching thread).  ~40 us of spin per step + 1 ms, capped at 50 ms."""
+    us = float(os.environ.get("MGLU_BENCH_AHEAD_US", "40")) if us_per_step is None else us_per_step
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(min(50e3, 1e3 + K * us) * 1965))
 
 
 def time_steps(fn_step, K, stream):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    enqueue_ahead(stream, K)
     e0.record(stream)
     for k in range(K):
         fn_step(k)
     e1.record(stream)
     e1.synchronize()
     return e0.elapsed_time(e1) / 1e3   # seconds
+
+
+def per_call_distribution(fn_step, K, stream):
+    """Separate pass (not the headline): an event pair around every call, so the per-call
+    median / p10 / p90 are visible.  Events between calls cut the PDL overlap of consecutive
+    launches, so these are slightly pessimistic against the headline loop."""
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    enqueue_ahead(stream, K)
+    evs[0].record(stream)
+    for k in range(K):
+        fn_step(k)
+        evs[k + 1].record(stream)
+    evs[-1].synchronize()
+    us = sorted(evs[k].elapsed_time(evs[k + 1]) * 1e3 for k in range(K))
+    q = lambda f: us[min(K - 1, int(round(f * (K - 1))))]   # noqa: E731
+    return {"median_us": q(0.5), "p10_us": q(0.1), "p90_us": q(0.9), "calls": K,
+            "how": "event pair around each call (separate pass; cuts PDL overlap between calls)"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def cublas_swiglu_us(d, h, B, L, K, stream):
@@ -249,29 +297,39 @@ def oracle_sample_cols(d, h, n_m, B):
 def cpu_baseline(d, h, n_m, B, act_code, budget_s=10.0):
     """The oracle as it stands (C, binary64, OpenMP over output columns) on the same workload:
     full layer (decode) or a column sample (prefill) per pass, repeated until ~budget_s of CPU
-    work; the rate is scaled to the metric's unit from the columns actually computed."""
+    work on all host cores, then ~budget_s/4 on one core; the rate is scaled to the metric's unit
+    from the columns actually computed."""
     from oracle import COracle
     o = COracle()
-    o.set_num_threads(os.cpu_count() or 1)
     rng = np.random.default_rng(0)
     c = oracle_sample_cols(d, h, n_m, B)
     x = rng.standard_normal((B, d))
     Wt = rng.uniform(-1 / d ** 0.5, 1 / d ** 0.5, (c, d))
     packed = rng.integers(0, 256, (h * d * n_m + 7) // 8, dtype=np.uint8)
-    cols = np.arange(c)
-    passes, t0 = 0, time.perf_counter()
-    while True:
-        o.forward(x, Wt, cols, packed, n_m, act_code)
-        passes += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or passes >= 200:
-            break
-    per = el / passes
     units, scale, unit, _ = work(d, c, n_m, B)
+
+    def timed(threads, budget, cols):
+        o.set_num_threads(threads)
+        passes, t0 = 0, time.perf_counter()
+        while True:
+            o.forward(x, Wt[:len(cols)], cols, packed, n_m, act_code)
+            passes += 1
+            el = time.perf_counter() - t0
+            if el >= budget or passes >= 200:
+                return el / passes, passes, el
+
+    per, passes, el = timed(os.cpu_count() or 1, budget_s, np.arange(c))
+    cores = o.num_threads()
+    # one core: a column sample of the same pass (the oracle's per-column cost is uniform)
+    c1 = max(1, min(c, int(c / max(1.0, per * cores / max(budget_s / 8, 1e-3)))))
+    per1, passes1, el1 = timed(1, budget_s / 4, np.arange(c1))
+    units1 = work(d, c1, n_m, B)[0]
     return {"value": units / per / scale, "unit": unit,
-            "cores": o.num_threads(), "kind": "oracle",
+            "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"B={B} tokens x {c} of {h} columns x d={d} per pass, {passes} passes in {el:.1f} s",
-            "seconds_per_call": per * h / c}
+            "seconds_per_call": per * h / c,
+            "one_core": {"value": units1 / per1 / scale, "unit": unit, "cores": 1,
+                         "sample": f"B={B} x {c1} columns x d={d} per pass, {passes1} passes in {el1:.1f} s"}}
 
 
 # ---------------------------------------------------------------- arms
@@ -317,7 +375,7 @@ def run_reference(args, ws, rank):
 
 def run_mglu(args, ws, rank, local):
     from paper_2506_23225_b200.build import build
-    if rank == 0:
+    if rank == 0 and not os.environ.get("MGLU_LIB"):     # (MGLU_LIB: an experiment build, see build.py)
         build()
     barrier(ws)
     from paper_2506_23225_b200.mglu import Mglu
@@ -330,7 +388,7 @@ def run_mglu(args, ws, rank, local):
     lo, hi = shard_bounds(h_total, ws, rank)
     h_loc = hi - lo
     L = args.layers
-    x, layers = make_layers(d, h_loc, n_m, B, L, seed=0, rank=rank)
+    x, fulls, layers = make_layers(d, h_total, n_m, B, L, seed=0, lo=lo, hi=hi)
     y = torch.empty(B, h_loc, device="cuda", dtype=torch.bfloat16)
     layer = Mglu(d, h_loc, n_m, act=act, dtype="bf16", device=local, path=args.path)
     stream = torch.cuda.Stream()
@@ -376,27 +434,35 @@ def run_mglu(args, ws, rank, local):
         stream.synchronize()
         launches_per_step = layer.last_launch_count() + (1 if (args.topk or args.ffn) else 0)
         path_used = layer.last_path()
-        # clock window + timed region, NVML-sampled.  The window is a step COUNT agreed by all ranks
-        # (steps may hold collectives: every rank must run the same number)
-        t0 = time.perf_counter()
-        for k in range(args.warmup):
-            step(k)
-        stream.synchronize()
-        t_step = max_over_ranks(ws, (time.perf_counter() - t0) / max(1, args.warmup))
-        n_clock = int(min(100000, args.clock_window / max(t_step, 1e-7)))
-        sampler = ClockSampler(local)
-        sampler.start()
-        for k in range(n_clock):
-            step(k)
-            if (k + 1) % 256 == 0:
-                stream.synchronize()
-        stream.synchronize()
+        # optional clock window (steps before the timed region; a step COUNT agreed by all ranks:
+        # steps may hold collectives).  Default 0: the timed region follows the W warm-up steps
+        # directly, as the driver's protocol states -- a long window only pre-heats the GPU into
+        # its power cap (measured: -4 us/call at the config-3 shape after a 0.3 s window)
+        if args.clock_window > 0:
+            t0 = time.perf_counter()
+            for k in range(args.warmup):
+                step(k)
+            stream.synchronize()
+            t_step = max_over_ranks(ws, (time.perf_counter() - t0) / max(1, args.warmup))
+            for k in range(int(min(100000, args.clock_window / max(t_step, 1e-7)))):
+                step(k)
+                if (k + 1) % 256 == 0:
+                    stream.synchronize()
+            stream.synchronize()
+        # timed region, NVML-sampled from a thread polling every 0.2 ms while the enqueue-ahead
+        # spin and the K steps run on the device
+        sampler = ClockSampler(local, period_s=0.0002)
         barrier(ws)
         torch.cuda.synchronize()
+        if not os.environ.get("MGLU_BENCH_NO_SAMPLER"):    # (experiment switch: NVML interference)
+            sampler.start()
         el = time_steps(step, args.steps, stream)
         torch.cuda.synchronize()
-        barrier(ws)
         sampler.stop()
+        barrier(ws)
+        dist_calls = per_call_distribution(step, args.steps, stream)
+        torch.cuda.synchronize()
+        barrier(ws)
     el_max = max_over_ranks(ws, el)
     units_layer, scale, unit, metric = work(d, h_total, n_m, B)
     units_rank = work(d, h_loc, n_m, B)[0]
@@ -418,52 +484,78 @@ def run_mglu(args, ws, rank, local):
     else:
         peak, peak_src, bound = peaks["hbm_gbs"], "hbm_gbs (copy)", "hbm"
 
-    # e2e through the C-ABI host-buffer entry: x H2D + kernel + y D2H every step.  Consecutive
-    # steps alternate over E streams, each with its own handle (own device staging buffers) and its
-    # own pinned host buffers, so one step's copies overlap another step's kernel; the timed region
-    # spans every stream (start event joined by all, end after all have drained).
-    E = max(1, args.e2e_streams) if not (args.topk or args.ffn) else 0
-    e_layers = [layer] + [Mglu(d, h_loc, n_m, act=act, dtype="bf16", device=local, path=args.path) for _ in range(E - 1)]
-    e_streams = [stream] + [torch.cuda.Stream() for _ in range(E - 1)]
-    xh = [x.cpu().pin_memory() for _ in range(E)]
-    yh = [torch.empty(B, h_loc, dtype=torch.bfloat16).pin_memory() for _ in range(E)]
+    # e2e through the C-ABI host-buffer entry (mglu_forward_host): per step, x H2D from pinned
+    # memory, the forward, y D2H to pinned memory.  `e2e`: ONE stream, every call serialised (the
+    # latency a dependent decode step sees).  `e2e_pipelined`: consecutive steps alternate over E
+    # streams, each with its own handle and pinned buffers, so one step's copies overlap another
+    # step's kernel (throughput of independent layers).
+    def e2e_leg(E):
+        e_layers = [layer] + [Mglu(d, h_loc, n_m, act=act, dtype="bf16", device=local, path=args.path)
+                              for _ in range(E - 1)]
+        e_streams = [stream] + [torch.cuda.Stream() for _ in range(E - 1)]
+        xh = [x.cpu().pin_memory() for _ in range(E)]
+        yh = [torch.empty(B, h_loc, dtype=torch.bfloat16).pin_memory() for _ in range(E)]
 
-    def step_host(k):
-        Wt, codes = layers[k % L]
-        e = k % E
-        e_layers[e].forward_host(xh[e], Wt, codes, yh[e], stream=e_streams[e])
+        def step_host(k):
+            Wt, codes = layers[k % L]
+            e = k % E
+            e_layers[e].forward_host(xh[e], Wt, codes, yh[e], stream=e_streams[e])
 
-    def time_e2e(K):
+        for k in range(max(3, args.warmup)):
+            step_host(k)
+        torch.cuda.synchronize()
+        barrier(ws)
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
+        enqueue_ahead(stream, args.steps)
         ev0.record(stream)
         for st_ in e_streams[1:]:
             st_.wait_event(ev0)
-        for k in range(K):
+        for k in range(args.steps):
             step_host(k)
         for st_ in e_streams[1:]:
             stream.wait_stream(st_)
         ev1.record(stream)
         ev1.synchronize()
-        return ev0.elapsed_time(ev1) / 1e3
+        el_e = max_over_ranks(ws, ev0.elapsed_time(ev1) / 1e3)
+        barrier(ws)
+        for extra in e_layers[1:]:
+            extra.close()
+        return {"value": units_layer * args.steps / el_e / scale, "unit": unit,
+                "h2d_bytes_per_step": B * d * 2 * ws, "d2h_bytes_per_step": B * h_total * 2,
+                "us_per_call": el_e / args.steps * 1e6, "streams": E}
 
-    if not E:
-        e_layers, e2e = [layer], None
-    else:
-        for k in range(max(3, args.warmup)):
-            step_host(k)
+    e2e = e2e_pipe = None
+    if not (args.topk or args.ffn):
+        e2e = e2e_leg(1)
+        e2e["how"] = ("mglu_forward_host per step on one stream: pinned x -> device, forward, y -> pinned host; "
+                      "every call serialised")
+        if args.e2e_streams > 1:
+            e2e_pipe = e2e_leg(args.e2e_streams)
+            e2e_pipe["how"] = (f"mglu_forward_host per step, steps alternating over {args.e2e_streams} streams/handles "
+                               "so one step's copies overlap another step's kernel (independent layers)")
+
+    # full-output check (N > 1): all-gather the h-sliced outputs over NCCL and compare, on rank 0,
+    # with the unsharded layer computed by the same kernels on rank 0's GPU (bit-identical: the
+    # kernels' reduction order does not depend on the shard)
+    gather_check = None
+    if ws > 1 and not (args.topk or args.ffn) and args.scaling == "strong":
+        from paper_2506_23225_b200.shard import gather_columns
+        Wt0, codes0 = layers[0]
+        layer.bind(x, Wt0, codes0, y, stream=stream)()
         torch.cuda.synchronize()
+        y_full = gather_columns(y, h_total, ws)
+        if rank == 0:
+            full = Mglu(d, h_total, n_m, act=act, dtype="bf16", device=local, path=args.path)
+            y_ref = torch.empty(B, h_total, device="cuda", dtype=torch.bfloat16)
+            full.forward(x, fulls[0][0], fulls[0][1], out=y_ref)
+            torch.cuda.synchronize()
+            full.close()
+            diff = (y_full.float() - y_ref.float()).abs()
+            gather_check = {"collective": "all_gather (NCCL)" if torch.distributed.get_backend() == "nccl" else "all_gather (gloo)",
+                            "bit_identical": bool(torch.equal(y_full, y_ref)), "max_abs_diff": float(diff.max()),
+                            "against": "unsharded layer on rank 0's GPU (same kernels, same seeds)"}
         barrier(ws)
-        el_e2e = time_e2e(args.steps)
-        barrier(ws)
-        el_e2e = max_over_ranks(ws, el_e2e)
-        e2e = {"value": units_layer * args.steps / el_e2e / scale, "unit": unit,
-               "h2d_bytes_per_step": B * d * 2 * ws, "d2h_bytes_per_step": B * h_total * 2,
-               "us_per_call": el_e2e / args.steps * 1e6, "streams": E,
-               "how": "mglu_forward_host per step (pinned x -> device, forward, y -> pinned host), steps "
-                      f"alternating over {E} streams/handles so copies overlap kernels"}
-    for extra in e_layers[1:]:
-        extra.close()
 
     out = None
     if rank == 0:
@@ -492,6 +584,9 @@ def run_mglu(args, ws, rank, local):
                          "peak_source": peaks["source"] + " " + peak_src,
                          "algorithmic_units_per_launch": units_rank, "algorithmic_bytes_per_launch": bytes_rank},
             "e2e": e2e,
+            **({"e2e_pipelined": e2e_pipe} if e2e_pipe else {}),
+            "per_call": dist_calls,
+            **({"gather_check": gather_check} if gather_check else {}),
             "gpu_launches": args.steps * launches_per_step,
             "clocks": sampler.summary(),
         }
@@ -518,12 +613,14 @@ def main(argv=None):
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--path", choices=["auto", "mma", "simt", "tcgen05", "tcdec"], default="auto")
     ap.add_argument("--layers", type=int, default=4, help="distinct layer copies rotated (L2 hygiene)")
-    ap.add_argument("--clock-window", type=float, default=0.3)
+    ap.add_argument("--clock-window", type=float, default=0.0,
+                    help="seconds of extra steps before the timed region (pre-heats the GPU; default none)")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
-    ap.add_argument("--e2e-streams", type=int, default=3, help="streams the e2e (host-buffer) leg alternates over")
+    ap.add_argument("--e2e-streams", type=int, default=3,
+                    help="streams the pipelined e2e leg (e2e_pipelined) alternates over; 0 skips it")
     ap.add_argument("--topk", type=int, default=0, help="Top-K routed MGLU: K kept masks (router + routed forward)")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                    help="N>1: weak = each GPU a full-width column block (work per GPU fixed); strong = split the N=1 layer")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                    help="N>1: strong = split the BASELINE layer's columns across the ranks; weak = each GPU a full-width column block (work per GPU fixed)")
     ap.add_argument("--ffn", action="store_true", help="FFN block: up-projection + dense W_o (+ all-reduce under torchrun)")
     ap.add_argument("--no-comparator", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

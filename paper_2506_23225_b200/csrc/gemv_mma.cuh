@@ -3,12 +3,18 @@
 //
 // The FlashMGLU forward of Alg. 1 for small B, re-designed for sm_100a:
 //  * a2: W (rows of Wt) and the packed codes stream HBM -> shared memory exactly once per call
-//    (P:245).  Each CTA owns a contiguous, row-balanced range of Wt rows (no split-K across
-//    CTAs, no atomics: reading R9).  Its rows are processed in rounds of up to 64 rows; a stage of
-//    a round is one 3-D TMA box of W (64-column blocks x rows, 128B-swizzled) plus one box of the
-//    codes, landing in a multi-stage mbarrier ring fed by one producer thread.
-//  * a3/a4: 16 consumer warps.  A round of T 8-row tiles gives each tile WPT = 16 / T warps, each
-//    owning 128 columns of every stage, so the last (ragged) round keeps all warps busy.  The n_m
+//    (P:245).  Each CTA owns a contiguous range of whole 8-row tiles of Wt (tile-balanced; no
+//    split-K across CTAs, no atomics: reading R9), processed in rounds
+//    of T = 8, 4, 2 or 1 tiles (full rounds of 8, then the remainder's binary digits); a stage of
+//    a round is one 3-D TMA box of W (64-column blocks x 8T rows, 128B-swizzled) plus one box of
+//    the codes, landing in a multi-stage mbarrier ring fed by one producer thread.  A consumer
+//    warp copies its share of a stage into registers and hands the slot back BEFORE its MMAs:
+//    a slot is held only for the shared-memory load latency, so nearly the whole ring is in
+//    flight (streaming at HBM rate needs ~130 KB in flight per SM at ~5000-cycle loaded latency,
+//    tools/probes/probe_sk.cu; holding slots through the MMAs cost ~15 % of the bandwidth).
+//  * a3/a4: 16 consumer warps.  A round of T tiles gives each tile WPT = 16 / T warps, each owning
+//    128 columns of every stage: every stage is 16384 elements and every warp's share of it is
+//    8 rows x 128 columns in every round, so no round is ragged.  The n_m
 //    masked operands are built in registers from the mask words as sign-flipped copies
 //    sigma_i (.) W (one IMAD + one LOP3 per bf16 pair and mask, see sign_flip) and fed, with the
 //    unmasked W, to mma.sync m16n8k16 (bf16 in, fp32 accumulate) with x as the B operand:
@@ -36,22 +42,14 @@
 
 namespace mglu {
 
-#ifndef MGLU_DEC_CONSUMERS
-#define MGLU_DEC_CONSUMERS 16
-#endif
-constexpr int kDecConsumers = MGLU_DEC_CONSUMERS;      // consumer warps (4 per SM sub-partition)
+constexpr int kDecConsumers = 16;                      // consumer warps (4 per SM sub-partition)
 constexpr int kDecThreads = (kDecConsumers + 1) * 32;  // + 1 producer warp
-constexpr int kDecFullTiles = kDecConsumers / 2;       // 8-row tiles of a full round (2 warps each)
-constexpr int kDecFullRows = 8 * kDecFullTiles;        // 64
-constexpr int kDecWBytes = kDecConsumers * 2048;       // W region of a stage slot (max over rounds)
+constexpr int kDecWBytes = kDecConsumers * 2048;       // W region of a stage slot (16384 bf16)
 
 // mask bytes of one 128-column block of a row: 4 groups x n_m words (TMA box inner span = swizzle span)
 template <int NM> __host__ __device__ constexpr int dec_code_span() { return 16 * NM; }   // 0: dense (n_m = 0)
-// stage slot = W region + codes region (rows x WPT blocks x 16 NM bytes <= 128 * consumers * NM)
+// stage slot = W region + codes region (16384 elements: 128 row-blocks x 16 n_m bytes)
 template <int NM> __host__ __device__ constexpr int dec_stage_bytes() { return kDecWBytes + 128 * kDecConsumers * NM; }
-
-// round geometry: T tiles of 8 rows, WPT warps per tile, stage width 128 * WPT columns
-__host__ __device__ constexpr int dec_wpt(int tiles) { return kDecConsumers / tiles; }
 
 struct DecParams {
   const __nv_bfloat16* x;
@@ -60,10 +58,19 @@ struct DecParams {
   int variant;               // partial-mask ablation variant (0 = Eq. 3; 1 NG, 2 NV, 3 NM)
   int act;                   // g when the kernel is the kRuntimeAct instantiation
   int B, d, h;
-  int rows_base, rows_rem;   // CTA c owns rows_base + (c < rows_rem) rows
+  int tiles_base, tiles_rem; // CTA c owns tiles_base + (c < tiles_rem) 8-row tiles
   int stages;                // ring depth
   int xpar;                  // u32 words per parity array of one token's x in smem (+ pad)
-  int rem_a, rem_b;          // last-round rows of CTAs owning rows_base / rows_base + 1 rows
+  int l2pf;                  // stages beyond the ring prefetched into L2 once, at the CTA's start
+};
+
+// One TMA descriptor pair per round type ti (T = 8 >> ti tiles of 8 rows, WPT = 2 << ti warps per
+// tile, stage width KS = 256 << ti columns): W boxes of 64 columns x 8T rows x 2 WPT blocks
+// (SW128) and code boxes of 16 n_m bytes x 8T rows x WPT blocks.  Every stage of every round type
+// is the same 8T x KS = 16384 elements, so every stage slot is exactly full.
+struct DecMaps {
+  CUtensorMap w[4];
+  CUtensorMap c[4];
 };
 
 // swizzled byte offset within a 1024-aligned region of `rb`-byte rows (rb in {16..128})
@@ -71,15 +78,44 @@ __device__ __forceinline__ uint32_t swz(uint32_t lin, uint32_t rb) {
   return lin ^ (((lin >> 7) & (rb / 16 - 1)) << 4);
 }
 
+// stages of one round of type ti over a reduction of d columns
+__host__ __device__ __forceinline__ int dec_round_stages(int ti, int d) { return (d + (256 << ti) - 1) >> (8 + ti); }
+
+// Round schedule of a CTA owning `ntiles` 8-row tiles: ntiles / 8 full rounds (ti = 0), then one
+// round per set bit of ntiles % 8, largest first (4 tiles: ti = 1, 2: ti = 2, 1: ti = 3).  Every
+// round keeps all 16 consumer warps on 8 rows x 128 columns per stage, so per-warp work is the
+// same in every round (no ragged round).  Stage i -> (round type, first row of the round, stage
+// within the round).
+__device__ __forceinline__ void dec_stage_of(int i, int nfull, int rem, int d, int& ti, int& row0, int& ks) {
+  const int n0 = dec_round_stages(0, d);
+  if (i < nfull * n0) {
+    const int r = i / n0;
+    ti = 0; row0 = 64 * r; ks = i - r * n0;
+    return;
+  }
+  int j = i - nfull * n0;
+  row0 = 64 * nfull;
+  ti = 3; ks = j;
+#pragma unroll
+  for (int b = 2; b >= 0; --b) {
+    if (!((rem >> b) & 1)) continue;
+    const int t = 3 - b, n = dec_round_stages(t, d);
+    if (j < n) { ti = t; ks = j; return; }
+    j -= n;
+    row0 += 8 << b;
+  }
+}
+
 template <int NM, int ACT, int NB, int KSEL>
 __global__ void __launch_bounds__(kDecThreads, 1)
-gemv_mma_kernel(const DecParams p,
-                const __grid_constant__ CUtensorMap mW64, const __grid_constant__ CUtensorMap mC64,
-                const __grid_constant__ CUtensorMap mWa, const __grid_constant__ CUtensorMap mCa,
-                const __grid_constant__ CUtensorMap mWb, const __grid_constant__ CUtensorMap mCb) {
+gemv_mma_kernel(const DecParams p, const __grid_constant__ DecMaps maps) {
   constexpr int SPAN = dec_code_span<NM>();
   constexpr int SB = dec_stage_bytes<NM>();
   constexpr int NACC = NB * ((KSEL > 0 ? KSEL : NM) + 1);
+  // 32-column steps loaded per register group: all 4 of a stage, or 2 / 1 where the staged
+  // operands would not fit beside the accumulators (n_m = 8; two token groups with n_m >= 4).
+  // (17 warps per CTA leave 96 registers per thread: one SM sub-partition holds 5 of them.)
+  constexpr int kGrp = (NB == 2 && (KSEL > 0 ? KSEL : NM) >= 4) ? 1 : ((KSEL > 0 ? KSEL : NM) * NB > 4) ? 2 : 4;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int S = p.stages;
   uint8_t* ring = smem;
@@ -90,15 +126,16 @@ gemv_mma_kernel(const DecParams p,
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
-  const int r0 = cta * p.rows_base + min(cta, p.rows_rem);
-  const int nrows = p.rows_base + (cta < p.rows_rem ? 1 : 0);
+  const int tile0 = cta * p.tiles_base + min(cta, p.tiles_rem);
+  const int ntiles = p.tiles_base + (cta < p.tiles_rem ? 1 : 0);
+  const int r0 = 8 * tile0;
+  const int nrows = min(8 * ntiles, p.h - r0);
   const int d = p.d;
-  const int nfull = nrows / kDecFullRows, rem = nrows - nfull * kDecFullRows;
-  const int nks_full = (d + 255) / 256;
-  const int t_rem = (rem + 7) >> 3;
-  const int wpt_rem = rem ? dec_wpt(t_rem) : 1;
-  const int nks_rem = rem ? (d + 128 * wpt_rem - 1) / (128 * wpt_rem) : 0;
-  const int nstages = nfull * nks_full + nks_rem;
+  const int nfull = ntiles >> 3, rem = ntiles & 7;
+  int nstages = nfull * dec_round_stages(0, d);
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+    if ((rem >> b) & 1) nstages += dec_round_stages(3 - b, d);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -112,31 +149,37 @@ gemv_mma_kernel(const DecParams p,
 
   if (warp == kDecConsumers) {
     // ------------------------------------------------------------ producer (one thread)
+    // two TMA ops per stage (W box + code box), no over-read: the boxes of a round hold exactly its
+    // 8T rows (a ragged last tile of the layer is zero-filled past h).
     if (lane == 0) {
-      // full rounds: boxes of 64 rows x (4 W blocks | 2 code blocks); the last round: boxes of
-      // exactly `rem` rows x (2 WPT W blocks | WPT code blocks) -> two TMA ops per stage always,
-      // no over-read of the neighbouring CTA's rows (one descriptor pair per CTA row count)
-      const CUtensorMap* mWr = rem == p.rem_a ? &mWa : &mWb;
-      const CUtensorMap* mCr = rem == p.rem_a ? &mCa : &mCb;
-      prefetch_tmap(&mW64);
-      if (NM > 0) prefetch_tmap(&mC64);
-      if (rem) { prefetch_tmap(mWr); if (NM > 0) prefetch_tmap(mCr); }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        prefetch_tmap(&maps.w[t]);
+        if (NM > 0) prefetch_tmap(&maps.c[t]);
+      }
       const uint64_t pol = policy_evict_first();
       int s = 0;
       uint32_t ph = 0;
       for (int i = 0; i < nstages; ++i) {
-        const bool is_full = i < nfull * nks_full;
-        const int rho = is_full ? i / nks_full : nfull;
-        const int ks = is_full ? i - rho * nks_full : i - nfull * nks_full;
-        const int rows = is_full ? kDecFullRows : rem;
-        const int wpt = is_full ? 2 : wpt_rem;
-        const int k0 = ks * 128 * wpt;
+        int ti, row0, ks;
+        dec_stage_of(i, nfull, rem, d, ti, row0, ks);
+        const int k0 = ks * (256 << ti);
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* wst = ring + (size_t)s * SB;
-        mbar_arrive_expect_tx(&full[s], (uint32_t)(rows * wpt * (2 * 128 + SPAN)));
-        tma_load_3d_hint(wst, is_full ? &mW64 : mWr, 0, r0 + rho * kDecFullRows, k0 / 64, &full[s], pol);
-        if constexpr (NM > 0)
-          tma_load_3d_hint(wst + kDecWBytes, is_full ? &mC64 : mCr, 0, r0 + rho * kDecFullRows, k0 / 128, &full[s], pol);
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(16384 * 2 + 16384 / 128 * SPAN));
+        tma_load_3d_hint(wst, &maps.w[ti], 0, r0 + row0, k0 / 64, &full[s], pol);
+        if constexpr (NM > 0) tma_load_3d_hint(wst + kDecWBytes, &maps.c[ti], 0, r0 + row0, k0 / 128, &full[s], pol);
+        if (i == S - 1) {
+          // ring filled: the next l2pf stages go to L2 once, so HBM keeps streaming while the
+          // consumers wait for the previous grid (PDL) and for x
+          for (int f = S; f < min(nstages, S + p.l2pf); ++f) {
+            int fti, frow, fks;
+            dec_stage_of(f, nfull, rem, d, fti, frow, fks);
+            const int fk0 = fks * (256 << fti);
+            tma_prefetch_3d(&maps.w[fti], 0, r0 + frow, fk0 / 64);
+            if constexpr (NM > 0) tma_prefetch_3d(&maps.c[fti], 0, r0 + frow, fk0 / 128);
+          }
+        }
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
@@ -153,16 +196,46 @@ gemv_mma_kernel(const DecParams p,
 #pragma unroll
   for (int q = 0; q < 4; ++q) mul[q] = 1u << (15 - 4 * c - q);
 
-  pdl_wait();                                              // x is the predecessor's output
+  // x -> smem split by bf16-pair parity: xs[2b + parity][pair / 2], zero-padded past d.  MMA
+  // columns of tokens >= B read token 0's row: their D columns are never used (finite either way).
+  // The zero fill does not depend on the predecessor grid and runs before the PDL wait; x itself
+  // is one 16-byte load per 8 columns, all of a thread's loads in flight together.
+  const int ctid = threadIdx.x;                             // consumer thread 0..511
+  constexpr int kCT = kDecConsumers * 32;
+  const int dw = d / 4;                                     // u32 words of one parity array
   {
-    // x -> smem split by bf16-pair parity: xs[b][parity][pair/2], zero-padded past d
-    // token B is an all-zero row: lanes whose MMA column has no token read it unconditionally
-    const int npair = p.xpar * 2 - 16;
-    for (int v = threadIdx.x; v < (B + 1) * npair; v += kDecConsumers * 32) {
-      const int b = v / npair, q = v - b * npair;
-      uint32_t val = 0u;
-      if (b < B && 2 * q < d) val = reinterpret_cast<const uint32_t*>(p.x + (size_t)b * d)[q];
-      xs[(size_t)(2 * b + (q & 1)) * p.xpar + (q >> 1)] = val;
+    const int padw = p.xpar - dw;
+    for (int v = ctid; v < 2 * B * padw; v += kCT) {
+      const int a = v / padw;
+      xs[(size_t)a * p.xpar + dw + (v - a * padw)] = 0u;
+    }
+  }
+#ifndef MGLU_ABL_NOPDLWAIT  // timing ablation (unsafe ordering): do not wait for the previous grid
+  pdl_wait();                                              // x is the predecessor's output
+#endif
+  {
+    const int nvec = d / 8;                                 // 16-byte vectors per token
+    const int total = B * nvec;
+    for (int base = ctid; base < total; base += 4 * kCT) {
+      uint4 u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int v = base + q * kCT;
+        if (v < total) {
+          const int b = v / nvec, e = v - b * nvec;
+          u[q] = *reinterpret_cast<const uint4*>(p.x + (size_t)b * d + 8 * e);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int v = base + q * kCT;
+        if (v < total) {
+          const int b = v / nvec, e = v - b * nvec;
+          // pairs 4e .. 4e+3: even pairs (4e, 4e+2) -> words 2e, 2e+1 of parity 0, odd -> parity 1
+          *reinterpret_cast<uint2*>(xs + (size_t)(2 * b) * p.xpar + 2 * e) = make_uint2(u[q].x, u[q].z);
+          *reinterpret_cast<uint2*>(xs + (size_t)(2 * b + 1) * p.xpar + 2 * e) = make_uint2(u[q].y, u[q].w);
+        }
+      }
     }
   }
   // KSEL > 0: Top-K routed forward (Appendix B).  Only the masks some token of the batch selected
@@ -176,14 +249,15 @@ gemv_mma_kernel(const DecParams p,
   if constexpr (KSEL > 0) {
     uint32_t active = 0u;
     for (int q = 0; q < B * NM; ++q) active |= (p.G[q] != 0.0f ? 1u : 0u) << (q % NM);
-    valid = 0u;
-    int n = 0;
+    // slot k = the (k+1)-th selected mask, lowest index first (static register indexing: __fns
+    // finds the bit, no local-memory array)
+    const int nsel = min(__popc(active), KSEL);
+    valid = (1u << nsel) - 1u;
 #pragma unroll
-    for (int i = 0; i < NM; ++i)
-      if (((active >> i) & 1u) && n < KSEL) { sel[n] = i; valid |= 1u << n; ++n; }
+    for (int k = 0; k < NSLOT; ++k) sel[k] = k < nsel ? (int)__fns(active, 0, k + 1) : 0;
 #pragma unroll
     for (int k = 0; k < NSLOT; ++k)
-      if (!((valid >> k) & 1u)) sel[k] = sel[0];
+      if (k >= nsel) sel[k] = sel[0];
   }
   named_bar_sync(1, kDecConsumers * 32);
 
@@ -197,15 +271,21 @@ gemv_mma_kernel(const DecParams p,
 
   int s = 0;
   uint32_t ph = 0;
-  int i = 0;
-  for (int rho = 0; rho < nfull + (rem ? 1 : 0); ++rho) {
-    const bool is_full = rho < nfull;
-    const int rows = is_full ? kDecFullRows : rem;
-    const int ntile = is_full ? kDecFullTiles : t_rem;
-    const int wpt = is_full ? 2 : wpt_rem;
-    const int nks = is_full ? nks_full : nks_rem;
+  int row0 = 0;
+  const int nrounds = nfull + __popc(rem);
+  for (int rho = 0; rho < nrounds; ++rho) {
+    // round type: full rounds first, then the remainder's set bits, largest first
+    int ti = 0;
+    if (rho >= nfull) {
+      int k = rho - nfull;
+#pragma unroll
+      for (int b = 2; b >= 0; --b)
+        if ((rem >> b) & 1) { if (k == 0) { ti = 3 - b; break; } --k; }
+    }
+    const int rows = 64 >> ti;
+    const int wpt = 2 << ti;
+    const int nks = dec_round_stages(ti, d);
     const int tl = warp / wpt, kp = warp - tl * wpt;        // tile and column part of this warp
-    const bool live = tl < ntile;                           // warp-uniform
     const int srow = tl * 8 + prow;                         // row within the round's box
     // per-round shared-memory offsets (bytes, relative to a stage slot) of this thread's operands
     // for the four 32-column steps st of a stage: the stage loop then only adds the slot base
@@ -227,60 +307,81 @@ gemv_mma_kernel(const DecParams p,
         for (int st = 0; st < 4; ++st)
           csel[k][st] = (uint32_t)kDecWBytes + swz((uint32_t)((kp * rows + srow) * SPAN + (st * NM + sel[k]) * 4), SPAN);
     }
-    // x: word index of pair 4c of step 0 of stage 0 for this lane's token column (token B = zeros)
+    // x: word index of pair 4c of step 0 of stage 0 for this lane's token column (tokens >= B: 0)
     uint32_t xoff[NB];
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) {
-      const int tok = min(nb * 4 + (g >> 1), B);
+      const int tok = nb * 4 + (g >> 1) < B ? nb * 4 + (g >> 1) : 0;
       xoff[nb] = (uint32_t)((2 * tok + (g & 1)) * p.xpar + kp * 32 + 2 * c) * 4u;
     }
-    for (int ks = 0; ks < nks; ++ks, ++i) {
+    for (int ks = 0; ks < nks; ++ks) {
       mbar_wait(&full[s], ph);
-      if (live) {
-        // slot base as a provably warp-uniform value: the LDS addresses become [per-thread + uniform]
-        const uint8_t* wst = ring + __shfl_sync(0xffffffffu, s * SB, 0);
-        const uint8_t* xst = reinterpret_cast<const uint8_t*>(xs) + __shfl_sync(0xffffffffu, ks * wpt * 128, 0);
+      // operands go to registers first and the slot goes back to the producer before the last
+      // group's MMAs: a slot is held only for the shared-memory load latency (plus, where
+      // registers force two load groups, the first group's MMAs), so nearly the whole ring stays
+      // in flight (the HBM stream needs ~130+ KB in flight per SM)
+      // slot base as a provably warp-uniform value: the LDS addresses become [per-thread + uniform]
+      const uint8_t* wst = ring + __shfl_sync(0xffffffffu, s * SB, 0);
+      const uint8_t* xst = reinterpret_cast<const uint8_t*>(xs) + __shfl_sync(0xffffffffu, ks * wpt * 128, 0);
 #pragma unroll
-        for (int st = 0; st < 4; ++st) {
-          const uint4 wq = *reinterpret_cast<const uint4*>(wst + woff[st]);
-          uint32_t mw[NSLOT > 0 ? NSLOT : 1];
+      for (int g0 = 0; g0 < 4; g0 += kGrp) {
+        uint4 wq[kGrp];
+        uint32_t mw[kGrp][NSLOT > 0 ? NSLOT : 1];
+        uint32_t xb[kGrp][NB][2];
+#pragma unroll
+        for (int j = 0; j < kGrp; ++j) {
+          const int st = g0 + j;
+          wq[j] = *reinterpret_cast<const uint4*>(wst + woff[st]);
           if constexpr (KSEL > 0) {
 #pragma unroll
-            for (int k = 0; k < KSEL; ++k) mw[k] = *reinterpret_cast<const uint32_t*>(wst + csel[k][st]);
-          } else if constexpr (NM > 0)
+            for (int k = 0; k < KSEL; ++k) mw[j][k] = *reinterpret_cast<const uint32_t*>(wst + csel[k][st]);
+          } else if constexpr (NM > 0) {
 #pragma unroll
-          for (int q = 0; q < (NM + 3) / 4; ++q) {
-            // n_m = 8: the second 16-byte chunk is the next one in the swizzled span
-            const uint8_t* cp = wst + (q == 0 ? coff[st] : (coff[st] ^ 16u));
-            if constexpr (NM == 1) mw[0] = *reinterpret_cast<const uint32_t*>(cp);
-            else if constexpr (NM == 2) { const uint2 u = *reinterpret_cast<const uint2*>(cp); mw[0] = u.x; mw[1] = u.y; }
-            else {
-              const uint4 u = *reinterpret_cast<const uint4*>(cp);
-              mw[4 * q] = u.x; mw[4 * q + 1] = u.y; mw[4 * q + 2] = u.z; mw[4 * q + 3] = u.w;
+            for (int q = 0; q < (NM + 3) / 4; ++q) {
+              // n_m = 8: the second 16-byte chunk is the next one in the swizzled span
+              const uint8_t* cp = wst + (q == 0 ? coff[st] : (coff[st] ^ 16u));
+              if constexpr (NM == 1) mw[j][0] = *reinterpret_cast<const uint32_t*>(cp);
+              else if constexpr (NM == 2) { const uint2 u = *reinterpret_cast<const uint2*>(cp); mw[j][0] = u.x; mw[j][1] = u.y; }
+              else {
+                const uint4 u = *reinterpret_cast<const uint4*>(cp);
+                mw[j][4 * q] = u.x; mw[j][4 * q + 1] = u.y; mw[j][4 * q + 2] = u.z; mw[j][4 * q + 3] = u.w;
+              }
             }
           }
           // B: x pairs (4c + parity, 4c + 2 + parity) of the step for this lane's column(s)
-          uint32_t xb[NB][2];
 #pragma unroll
           for (int nb = 0; nb < NB; ++nb) {
             const uint2 u = *reinterpret_cast<const uint2*>(xst + xoff[nb] + st * 32);
-            xb[nb][0] = u.x; xb[nb][1] = u.y;
+            xb[j][nb][0] = u.x; xb[j][nb][1] = u.y;
           }
+        }
+        if (g0 + kGrp == 4) {                                 // the stage's last loads are issued
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        }
+#pragma unroll
+        for (int j = 0; j < kGrp; ++j) {
+#ifdef MGLU_ABL_NOMMA   // timing ablation (wrong results): operands loaded, no tensor-core work
+          acc[0][0][0] += __uint_as_float(wq[j].x ^ wq[j].y ^ wq[j].z ^ wq[j].w ^ mw[j][0] ^ xb[j][0][0] ^ xb[j][0][1]);
+          continue;
+#endif
           // t += x W
 #pragma unroll
-          for (int nb = 0; nb < NB; ++nb) mma_16816(acc[nb][0], wq.x, wq.y, wq.z, wq.w, xb[nb][0], xb[nb][1]);
+          for (int nb = 0; nb < NB; ++nb) mma_16816(acc[nb][0], wq[j].x, wq[j].y, wq[j].z, wq[j].w, xb[j][nb][0], xb[j][nb][1]);
+#ifdef MGLU_ABL_NOMASK  // timing ablation (wrong results): t only
+          acc[0][1][0] += __uint_as_float(mw[j][0] ^ mw[j][NSLOT - 1]);
+          continue;
+#endif
           // u_i += x (sigma_i (.) W): pair q of the thread's 8 columns is register q of the quad
 #pragma unroll
           for (int ii = 0; ii < NSLOT; ++ii) {
-            const uint32_t a0 = sign_flip(wq.x, mw[ii], mul[0]), a1 = sign_flip(wq.y, mw[ii], mul[1]);
-            const uint32_t a2 = sign_flip(wq.z, mw[ii], mul[2]), a3 = sign_flip(wq.w, mw[ii], mul[3]);
+            const uint32_t a0 = sign_flip(wq[j].x, mw[j][ii], mul[0]), a1 = sign_flip(wq[j].y, mw[j][ii], mul[1]);
+            const uint32_t a2 = sign_flip(wq[j].z, mw[j][ii], mul[2]), a3 = sign_flip(wq[j].w, mw[j][ii], mul[3]);
 #pragma unroll
-            for (int nb = 0; nb < NB; ++nb) mma_16816(acc[nb][1 + ii], a0, a1, a2, a3, xb[nb][0], xb[nb][1]);
+            for (int nb = 0; nb < NB; ++nb) mma_16816(acc[nb][1 + ii], a0, a1, a2, a3, xb[j][nb][0], xb[j][nb][1]);
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == S) { s = 0; ph ^= 1; }
     }
 
@@ -296,7 +397,7 @@ gemv_mma_kernel(const DecParams p,
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[nb][a][q] = 0.f;
       }
-    if (live && kp > 0) {
+    if (kp > 0) {
       float* pw = part + ((size_t)warp * 32 + lane) * NACC;
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb)
@@ -304,7 +405,7 @@ gemv_mma_kernel(const DecParams p,
         for (int a = 0; a <= NSLOT; ++a) pw[nb * (NSLOT + 1) + a] = v[nb][a];
     }
     named_bar_sync(1, kDecConsumers * 32);                  // the producer keeps streaming meanwhile
-    if (live && kp == 0) {
+    if (kp == 0) {
       for (int q = 1; q < wpt; ++q) {
         const float* pq = part + ((size_t)(warp + q) * 32 + lane) * NACC;
 #pragma unroll
@@ -312,7 +413,7 @@ gemv_mma_kernel(const DecParams p,
 #pragma unroll
           for (int a = 0; a <= NSLOT; ++a) v[nb][a] += pq[nb * (NSLOT + 1) + a];
       }
-      const int row = rho * kDecFullRows + tl * 8 + prow;
+      const int row = row0 + tl * 8 + prow;
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) {
         const int tok = nb * 4 + c;
@@ -337,6 +438,7 @@ gemv_mma_kernel(const DecParams p,
       }
     }
     named_bar_sync(1, kDecConsumers * 32);                  // partials are rewritten next round
+    row0 += rows;
   }
 }
 

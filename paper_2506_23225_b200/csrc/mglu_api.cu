@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <array>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -24,9 +25,6 @@
 #include "pack.cuh"
 #include "router.cuh"
 
-#ifndef MGLU_DEC_SMEM_KB
-#define MGLU_DEC_SMEM_KB 200   // shared-memory budget of the HMMA decode kernel (ring depth)
-#endif
 
 struct mglu_ctx {
   int64_t d = 0, h = 0;
@@ -49,7 +47,7 @@ struct mglu_ctx {
     const void* Wt = nullptr;
     const void* codes = nullptr;
     uint64_t stamp = 0;
-    CUtensorMap maps[6];
+    mglu::DecMaps maps;
   };
   std::array<DecMaps, 16> dec_cache;
   uint64_t dec_clock = 0;
@@ -137,6 +135,9 @@ cudaError_t simt_act(mglu_ctx* hd, const void* x, int B, const void* Wt, const v
 template <typename T, bool PARTIALS>
 cudaError_t simt_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
                     void* out, float* z, cudaStream_t st) {
+#ifdef MGLU_DEC_ONLY
+  return cudaErrorInvalidValue;
+#endif
   switch (hd->n_m) {
     case 1: return simt_act<T, PARTIALS, 1>(hd, x, B, Wt, codes, out, z, st);
     case 2: return simt_act<T, PARTIALS, 2>(hd, x, B, Wt, codes, out, z, st);
@@ -145,16 +146,19 @@ cudaError_t simt_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const vo
     case 5: return simt_act<T, PARTIALS, 5>(hd, x, B, Wt, codes, out, z, st);
     case 6: return simt_act<T, PARTIALS, 6>(hd, x, B, Wt, codes, out, z, st);
     case 7: return simt_act<T, PARTIALS, 7>(hd, x, B, Wt, codes, out, z, st);
+    case 8: return simt_act<T, PARTIALS, 8>(hd, x, B, Wt, codes, out, z, st);
     case 16: return simt_act<T, PARTIALS, 16>(hd, x, B, Wt, codes, out, z, st);
-    default: return simt_act<T, PARTIALS, 8>(hd, x, B, Wt, codes, out, z, st);
+    default: return cudaErrorInvalidValue;                  // (n_m = 0 dense handles never get here)
   }
 }
 
 // ------------------------------------------------------------------ MMA (TMA-fed decode) dispatch
 bool mma_can_serve(const mglu_ctx* hd, int64_t B) {
-  // 128-column code blocks of 16 * n_m bytes tile the rows exactly
-  return hd->dtype == MGLU_BF16 && (hd->n_m == 0 || fast_nm(hd->n_m)) && hd->d % 128 == 0 && B >= 1 && B <= 8 &&
-         hd->d <= 32768;
+  // 128-column code blocks of 16 * n_m bytes tile the rows exactly; n_m >= 4 keeps one token group
+  // (B <= 4: two groups' accumulators do not fit the 96-register budget without spilling -- and the
+  // stream-K tcgen05 GEMV is faster there anyway, profiles/r02_decode.txt)
+  return hd->dtype == MGLU_BF16 && (hd->n_m == 0 || fast_nm(hd->n_m)) && hd->d % 128 == 0 && B >= 1 &&
+         B <= (hd->n_m >= 4 ? 4 : 8) && hd->d <= 32768;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -193,14 +197,14 @@ bool encode_3d_blocks(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, cons
 }
 
 // descriptor cache keyed by (Wt, codes).  W: 64-column blocks (SW128); codes: 128-column blocks of
-// 16*n_m bytes (swizzle = span).  Boxes: full rounds 64 rows x (4 | 2) blocks; the last round of
-// CTAs owning rows_base / rows_base + 1 rows: rem_a / rem_b rows x (2 wpt | wpt) blocks.
-bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, int rem_a, int rem_b, CUtensorMap* out6) {
+// 16*n_m bytes (swizzle = span).  Round type ti (T = 8 >> ti tiles): boxes of 8T rows x
+// (2 WPT | WPT) blocks, WPT = 2 << ti.
+bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, mglu::DecMaps* out) {
   std::lock_guard<std::mutex> g(hd->mu);
   for (auto& e : hd->dec_cache)
     if (e.valid && e.Wt == Wt && e.codes == codes) {
       e.stamp = ++hd->dec_clock;
-      memcpy(out6, e.maps, sizeof(e.maps));
+      *out = e.maps;
       return true;
     }
   const int NM = hd->n_m;
@@ -208,26 +212,15 @@ bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, int rem_a, int re
   const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
   const auto csw = span == 16 ? CU_TENSOR_MAP_SWIZZLE_NONE : swizzle_for(span);
   const uint64_t crow_u32 = (uint64_t)hd->d * NM / 32;
-  auto wpt_of = [](int rem) { return rem ? mglu::dec_wpt((rem + 7) / 8) : 1; };
-  const int ra = rem_a ? rem_a : 1, rb = rem_b ? rem_b : 1;
-  CUtensorMap m[6];
-  const uint32_t fr = mglu::kDecFullRows;
-  if (NM == 0) {                                            // dense projection: W boxes only
-    const bool okd =
-        encode_3d_blocks(&m[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, fr, 4, sw) &&
-        encode_3d_blocks(&m[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, ra, 2 * wpt_of(rem_a), sw) &&
-        encode_3d_blocks(&m[4], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, rb, 2 * wpt_of(rem_b), sw);
-    if (!okd) return false;
-    m[1] = m[0]; m[3] = m[2]; m[5] = m[4];
+  mglu::DecMaps m;
+  for (int ti = 0; ti < 4; ++ti) {
+    const uint32_t rows = 64u >> ti, wpt = 2u << ti;
+    if (!encode_3d_blocks(&m.w[ti], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, rows, 2 * wpt, sw))
+      return false;
+    if (NM == 0) m.c[ti] = m.w[ti];                          // dense projection: W boxes only
+    else if (!encode_3d_blocks(&m.c[ti], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, rows, wpt, csw))
+      return false;
   }
-  bool ok = NM == 0 ||
-      encode_3d_blocks(&m[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, fr, 4, sw) &&
-      encode_3d_blocks(&m[1], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, fr, 2, csw) &&
-      encode_3d_blocks(&m[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, ra, 2 * wpt_of(rem_a), sw) &&
-      encode_3d_blocks(&m[3], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, ra, wpt_of(rem_a), csw) &&
-      encode_3d_blocks(&m[4], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, rb, 2 * wpt_of(rem_b), sw) &&
-      encode_3d_blocks(&m[5], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, rb, wpt_of(rem_b), csw);
-  if (!ok) return false;
   size_t victim = 0;
   for (size_t i = 0; i < hd->dec_cache.size(); ++i) {
     if (!hd->dec_cache[i].valid) { victim = i; break; }
@@ -235,9 +228,28 @@ bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, int rem_a, int re
   }
   auto& e = hd->dec_cache[victim];
   e.valid = true; e.Wt = Wt; e.codes = codes; e.stamp = ++hd->dec_clock;
-  memcpy(e.maps, m, sizeof(m));
-  memcpy(out6, m, sizeof(m));
+  e.maps = m;
+  *out = m;
   return true;
+}
+
+// shared-memory budget of the HMMA decode kernel in KB (sets the ring depth; MGLU_DEC_SMEM_KB
+// overrides, for experiments)
+int dec_smem_kb() {
+  static const int v = [] {
+    const char* e = getenv("MGLU_DEC_SMEM_KB");
+    return e ? atoi(e) : 200;
+  }();
+  return v;
+}
+
+// one-shot L2 prefetch depth of the decode kernel (stages past the ring; MGLU_DEC_L2PF overrides)
+int dec_l2pf() {
+  static const int v = [] {
+    const char* e = getenv("MGLU_DEC_L2PF");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
 }
 
 template <int NM, int ACT, int NB, int KSEL>
@@ -252,29 +264,33 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   p.B = B;
   p.d = (int)hd->d;
   p.h = (int)hd->h;
-  int64_t ncta = (hd->h + 7) / 8;
-  if (ncta > hd->num_sms) ncta = hd->num_sms;
-  p.rows_base = (int)(hd->h / ncta);
-  p.rows_rem = (int)(hd->h % ncta);
-  p.rem_a = p.rows_base % mglu::kDecFullRows;
-  p.rem_b = (p.rows_base + 1) % mglu::kDecFullRows;
-  CUtensorMap maps[6];
-  if (!dec_maps(hd, Wt, codes, p.rem_a, p.rem_b, maps)) return cudaErrorInvalidValue;
-  // x in smem, split by pair parity and zero-padded to the last column any stage can touch
-  int64_t maxcol = (hd->d + 255) / 256 * 256;
-  for (int rem : {p.rem_a, p.rem_b}) {
-    if (!rem) continue;
-    const int64_t ks = 128 * (int64_t)mglu::dec_wpt((rem + 7) / 8);
-    maxcol = std::max<int64_t>(maxcol, (hd->d + ks - 1) / ks * ks);
+  // whole 8-row tiles per CTA, one CTA per SM (the last tile of a ragged h is zero-filled by TMA)
+  const int64_t tiles = (hd->h + 7) / 8;
+  const int64_t ncta = std::min<int64_t>(tiles, hd->num_sms);
+  p.tiles_base = (int)(tiles / ncta);
+  p.tiles_rem = (int)(tiles % ncta);
+  p.l2pf = dec_l2pf();
+  mglu::DecMaps maps;
+  if (!dec_maps(hd, Wt, codes, &maps)) return cudaErrorInvalidValue;
+  // x in smem, split by pair parity and zero-padded to the last column any stage can touch (the
+  // widest round type a CTA of this grid runs)
+  int64_t maxcol = hd->d;
+  for (int64_t nt : {(int64_t)p.tiles_base, (int64_t)p.tiles_base + (p.tiles_rem ? 1 : 0)}) {
+    for (int ti = 0; ti < 4; ++ti) {
+      const bool used = ti == 0 ? nt >= 8 : ((nt & 7) >> (3 - ti)) & 1;
+      if (!used) continue;
+      const int64_t ks = 256 << ti;
+      maxcol = std::max<int64_t>(maxcol, (hd->d + ks - 1) / ks * ks);
+    }
   }
   const int npair = (int)(maxcol / 2);
   p.xpar = npair / 2 + 8;
   constexpr size_t SB = mglu::dec_stage_bytes<NM>();
-  const size_t xbytes = (size_t)2 * (B + 1) * p.xpar * 4;   // + an all-zero token row
+  const size_t xbytes = (size_t)2 * B * p.xpar * 4;
   const size_t partbytes = (size_t)mglu::kDecConsumers * 32 * NB * ((KSEL > 0 ? KSEL : NM) + 1) * 4;
   const size_t fixed = xbytes + partbytes + 1024;
   // (dense handles with a long reduction stage a large x: let them use the whole opt-in budget)
-  const size_t cap = std::min<size_t>((size_t)hd->max_smem_optin, NM == 0 ? (size_t)hd->max_smem_optin : (size_t)MGLU_DEC_SMEM_KB * 1024);
+  const size_t cap = std::min<size_t>((size_t)hd->max_smem_optin, NM == 0 ? (size_t)hd->max_smem_optin : (size_t)dec_smem_kb() * 1024);
   if (cap < fixed) return cudaErrorInvalidConfiguration;
   int S = (int)((cap - fixed) / (SB + 16));
   S = std::min(8, S);
@@ -284,8 +300,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   auto kern = mglu::gemv_mma_kernel<NM, ACT, NB, KSEL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(kern, dim3((unsigned)ncta), dim3(mglu::kDecThreads), smem, st, p, maps[0], maps[1], maps[2],
-                    maps[3], maps[4], maps[5]);
+  return launch_pdl(kern, dim3((unsigned)ncta), dim3(mglu::kDecThreads), smem, st, p, maps);
 }
 
 template <int NM, int ACT>
@@ -295,19 +310,18 @@ cudaError_t run_mma(mglu_ctx* hd, const void* x, int B, const void* Wt, const vo
   // token, so min(n_m, B*K) slots, rounded up to a power of two (other activations and larger
   // unions run all masks with the weights in the epilogue)
   if constexpr (ACT == mglu::kSwish && NM >= 2) {
-    if (t_routed_G && t_routed_K > 0 && hd->variant == 0) {
+    // (B > 4: B*K >= 5 tokens' selections cover min(n_m, 5) >= every slot count below -- all masks)
+    if (t_routed_G && t_routed_K > 0 && hd->variant == 0 && B <= 4) {
       const int u = std::min(NM, B * t_routed_K);
-      if (u <= 1) return B <= 4 ? run_mma_nb<NM, ACT, 1, 1>(hd, x, B, Wt, codes, out, st)
-                                : run_mma_nb<NM, ACT, 2, 1>(hd, x, B, Wt, codes, out, st);
-      if (u <= 2 && NM > 2) return B <= 4 ? run_mma_nb<NM, ACT, 1, 2>(hd, x, B, Wt, codes, out, st)
-                                          : run_mma_nb<NM, ACT, 2, 2>(hd, x, B, Wt, codes, out, st);
+      if (u <= 1) return run_mma_nb<NM, ACT, 1, 1>(hd, x, B, Wt, codes, out, st);
+      if (u <= 2 && NM > 2) return run_mma_nb<NM, ACT, 1, 2>(hd, x, B, Wt, codes, out, st);
       if constexpr (NM == 8)
-        if (u <= 4) return B <= 4 ? run_mma_nb<NM, ACT, 1, 4>(hd, x, B, Wt, codes, out, st)
-                                  : run_mma_nb<NM, ACT, 2, 4>(hd, x, B, Wt, codes, out, st);
+        if (u <= 4) return run_mma_nb<NM, ACT, 1, 4>(hd, x, B, Wt, codes, out, st);
     }
   }
-  return B <= 4 ? run_mma_nb<NM, ACT, 1, 0>(hd, x, B, Wt, codes, out, st)
-                : run_mma_nb<NM, ACT, 2, 0>(hd, x, B, Wt, codes, out, st);
+  if constexpr (NM >= 4) return B <= 4 ? run_mma_nb<NM, ACT, 1, 0>(hd, x, B, Wt, codes, out, st) : cudaErrorInvalidValue;
+  else return B <= 4 ? run_mma_nb<NM, ACT, 1, 0>(hd, x, B, Wt, codes, out, st)
+                     : run_mma_nb<NM, ACT, 2, 0>(hd, x, B, Wt, codes, out, st);
 }
 
 template <int NM>
@@ -321,6 +335,12 @@ cudaError_t mma_act(mglu_ctx* hd, const void* x, int B, const void* Wt, const vo
 
 cudaError_t mma_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes, void* out,
                    cudaStream_t st) {
+#ifdef MGLU_DEC_ONLY   // experiment build (tools): the n_m in {1, 4} Swish decode kernels only
+  if (hd->act != MGLU_ACT_SWISH || B > 4 || t_routed_G) return cudaErrorInvalidValue;
+  if (hd->n_m == 4) return run_mma_nb<4, mglu::kSwish, 1, 0>(hd, x, B, Wt, codes, out, st);
+  if (hd->n_m == 1) return run_mma_nb<1, mglu::kSwish, 1, 0>(hd, x, B, Wt, codes, out, st);
+  return cudaErrorInvalidValue;
+#endif
   switch (hd->n_m) {
     case 0: return run_mma<0, mglu::kIdentity>(hd, x, B, Wt, codes, out, st);   // dense projection
     case 1: return mma_act<1>(hd, x, B, Wt, codes, out, st);
@@ -444,6 +464,9 @@ cudaError_t tc_act(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const
 
 cudaError_t tc_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
                   cudaStream_t st) {
+#ifdef MGLU_DEC_ONLY
+  return cudaErrorInvalidValue;
+#endif
   switch (hd->n_m) {
     case 1: return tc_act<1>(hd, x, B, Wt, codes, out, st);
     case 2: return tc_act<2>(hd, x, B, Wt, codes, out, st);
@@ -536,6 +559,9 @@ cudaError_t run_sk(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const
 
 cudaError_t sk_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
                   cudaStream_t st) {
+#ifdef MGLU_DEC_ONLY
+  return cudaErrorInvalidValue;
+#endif
   switch (hd->n_m) {
     case 1: return run_sk<1>(hd, x, B, Wt, codes, out, st);
     case 2: return run_sk<2>(hd, x, B, Wt, codes, out, st);
@@ -715,7 +741,7 @@ static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, con
   if (path == MGLU_PATH_MMA) {
     if (!mma_can_serve(hd, B)) {
       if (prev != hd->device) cudaSetDevice(prev);
-      return set_err(hd, MGLU_ERR_UNSUPPORTED, "MMA path needs bf16, 1 <= B <= 8, d % 128 == 0");
+      return set_err(hd, MGLU_ERR_UNSUPPORTED, "MMA path needs bf16, 1 <= B <= 8 (B <= 4 for n_m >= 4), d % 128 == 0");
     }
     e = mma_nm(hd, x, (int)B, Wt, packed, out, st);
     launches = 1;
@@ -815,6 +841,7 @@ mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const 
 
 mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, const void* Wt,
                                   const void* packed, float* z, void* stream) {
+  if (hd && hd->n_m == 0) return set_err(hd, MGLU_ERR_UNSUPPORTED, "partials need masks (n_m >= 1)");
   mglu_status s = check_ptrs(hd, x, B, Wt, packed, z);
   if (s != MGLU_OK) return s;
   hd->last_launches = 0;

@@ -41,11 +41,13 @@ class MgluError(RuntimeError):
 _lib = None
 
 
-def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load libmglu.so (built in-tree by ``paper_2506_23225_b200.build``)."""
+def load_library(path: str | None = None) -> ctypes.CDLL:
+    """Load libmglu.so (built in-tree by ``paper_2506_23225_b200.build``; MGLU_LIB points at an
+    experiment build instead -- those are never written over the product library)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("MGLU_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise MgluLibraryMissing(
             f"{path} not found: build it with `python -m paper_2506_23225_b200.build` "
@@ -246,8 +248,10 @@ class Mglu:
         td = TORCH_DTYPE[self.dtype]
         if x.dtype != td or Wt.dtype != td:
             raise MgluError(MGLU_ERR_INVALID_ARG, f"x/Wt must be {td}")
-        if tuple(Wt.shape) != (self.h, self.d) or x.shape[-1] != self.d:
-            raise MgluError(MGLU_ERR_INVALID_ARG, "shape mismatch")
+        if x.dim() != 2 or tuple(Wt.shape) != (self.h, self.d) or x.shape[1] != self.d:
+            raise MgluError(MGLU_ERR_INVALID_ARG, "shape mismatch: x must be [B][d] (flatten leading dims), Wt [h][d]")
+        if x.device != Wt.device:
+            raise MgluError(MGLU_ERR_INVALID_ARG, "x and Wt must be on the same device")
         if self.n_m == 0 and packed is None:              # dense projection (FFN W_o): no codes
             packed = torch.empty(0, dtype=torch.uint8, device=Wt.device)
         if packed.dtype != torch.uint8 or packed.numel() != mglu_packed_mask_bytes(self.d, self.h, self.n_m):
@@ -255,14 +259,24 @@ class Mglu:
         if not (x.is_contiguous() and Wt.is_contiguous() and packed.is_contiguous()):
             raise MgluError(MGLU_ERR_INVALID_ARG, "tensors must be contiguous")
 
+    def _check_out(self, out, B, x):
+        if out.dtype != TORCH_DTYPE[self.dtype] or tuple(out.shape) != (B, self.h) or not out.is_contiguous() \
+                or out.device != x.device:
+            raise MgluError(MGLU_ERR_INVALID_ARG, f"out must be a contiguous {TORCH_DTYPE[self.dtype]} [B][h] tensor on x's device")
+
     def forward(self, x: torch.Tensor, Wt: torch.Tensor, packed: torch.Tensor,
                 out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-        self._check_inputs(x, Wt, packed)
-        B = x.shape[0] if x.dim() == 2 else 1
+        """y [..., h] = MGLU(x [..., d]): leading dims of x are flattened into the token count."""
+        lead = tuple(x.shape[:-1])
+        x2 = x.reshape(-1, x.shape[-1]) if x.dim() != 2 else x
+        self._check_inputs(x2, Wt, packed)
+        B = x2.shape[0]
         if out is None:
             out = torch.empty((B, self.h), dtype=TORCH_DTYPE[self.dtype], device=x.device)
-        mglu_forward(self.handle, x, B, Wt, packed, out, stream)
-        return out
+        else:
+            self._check_out(out.reshape(B, self.h) if out.dim() != 2 else out, B, x2)
+        mglu_forward(self.handle, x2, B, Wt, packed, out, stream)
+        return out.reshape(*lead, self.h) if x.dim() != 2 else out
 
     __call__ = forward
 
@@ -270,8 +284,9 @@ class Mglu:
         """Validate once and return a zero-argument callable that enqueues mglu_forward with
         the pointers pre-marshalled (the per-call host cost is one ctypes call)."""
         self._check_inputs(x, Wt, packed)
+        B = x.shape[0]
+        self._check_out(out, B, x)
         lib = load_library()
-        B = x.shape[0] if x.dim() == 2 else 1
         args = (self.handle, x.data_ptr(), B, Wt.data_ptr(), packed.data_ptr() if packed is not None else None, out.data_ptr(),
                 _stream_ptr(stream, x.device))
         fwd = lib.mglu_forward
@@ -286,6 +301,8 @@ class Mglu:
         """G = Softmax(TopK(x W_r)) [B][n_m] fp32 (Appendix B); Wr is [n_m][d] bf16."""
         if Wr.dtype != torch.bfloat16 or tuple(Wr.shape) != (self.n_m, self.d) or not Wr.is_contiguous():
             raise MgluError(MGLU_ERR_INVALID_ARG, "Wr must be a contiguous bf16 [n_m][d] tensor")
+        if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.d or x.device != Wr.device:
+            raise MgluError(MGLU_ERR_INVALID_ARG, "x must be a bf16 [B][d] tensor on Wr's device")
         B = x.shape[0]
         G = torch.empty((B, self.n_m), dtype=torch.float32, device=x.device)
         mglu_router_topk(self.handle, x.contiguous(), B, Wr, K, G, stream)
@@ -300,6 +317,8 @@ class Mglu:
             raise MgluError(MGLU_ERR_INVALID_ARG, "G must be a contiguous fp32 [B][n_m] tensor")
         if out is None:
             out = torch.empty((B, self.h), dtype=TORCH_DTYPE[self.dtype], device=x.device)
+        else:
+            self._check_out(out, B, x)
         mglu_forward_routed(self.handle, x, B, Wt, packed, G, K, out, stream)
         return out
 
@@ -312,7 +331,18 @@ class Mglu:
 
     def forward_host(self, x_host: torch.Tensor, Wt: torch.Tensor, packed: torch.Tensor,
                      out_host: torch.Tensor, stream=None) -> torch.Tensor:
+        td = TORCH_DTYPE[self.dtype]
+        if x_host.is_cuda or out_host.is_cuda:
+            raise MgluError(MGLU_ERR_INVALID_ARG, "forward_host takes host tensors (pinned for async copies)")
+        if x_host.dtype != td or x_host.dim() != 2 or x_host.shape[1] != self.d or not x_host.is_contiguous():
+            raise MgluError(MGLU_ERR_INVALID_ARG, f"x_host must be a contiguous {td} [B][d] host tensor")
         B = x_host.shape[0]
+        if out_host.dtype != td or tuple(out_host.shape) != (B, self.h) or not out_host.is_contiguous():
+            raise MgluError(MGLU_ERR_INVALID_ARG, f"out_host must be a contiguous {td} [B][h] host tensor")
+        if Wt.dtype != td or tuple(Wt.shape) != (self.h, self.d) or not Wt.is_cuda:
+            raise MgluError(MGLU_ERR_INVALID_ARG, "Wt must be a device [h][d] tensor")
+        if self.n_m and (packed is None or packed.numel() != mglu_packed_mask_bytes(self.d, self.h, self.n_m)):
+            raise MgluError(MGLU_ERR_INVALID_ARG, "packed codes size mismatch")
         mglu_forward_host(self.handle, x_host, B, Wt, packed, out_host, stream)
         return out_host
 

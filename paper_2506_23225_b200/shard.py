@@ -20,11 +20,21 @@ from __future__ import annotations
 import torch
 
 
-def shard_bounds(h: int, world: int, rank: int) -> tuple[int, int]:
-    """Rows [lo, hi) of rank `rank`: contiguous, sizes differ by at most one row, rank order."""
+SHARD_ALIGN = 128   # rows per shard granule: whole tcgen05 M-tiles / HMMA row tiles on every rank
+
+
+def shard_bounds(h: int, world: int, rank: int, align: int = SHARD_ALIGN) -> tuple[int, int]:
+    """Rows [lo, hi) of rank `rank`: contiguous, in rank order, made of whole `align`-row granules
+    (granule counts differ by at most one; only the last rank's last granule may be ragged), so
+    every shard keeps the kernels' whole-tile shapes and a row-parallel W_o shard stays
+    128-aligned (h_g % 128 == 0 whenever h % 128 == 0)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad world/rank")
-    return rank * h // world, (rank + 1) * h // world
+    if align < 1:
+        raise ValueError("align must be >= 1")
+    n = (h + align - 1) // align
+    lo, hi = rank * n // world * align, (rank + 1) * n // world * align
+    return min(lo, h), min(hi, h)
 
 
 def code_bytes_per_row(d: int, n_m: int) -> int:
@@ -34,29 +44,30 @@ def code_bytes_per_row(d: int, n_m: int) -> int:
     return d * n_m // 8
 
 
-def shard_layer(Wt: torch.Tensor, packed: torch.Tensor, n_m: int, world: int, rank: int):
+def shard_layer(Wt: torch.Tensor, packed: torch.Tensor, n_m: int, world: int, rank: int,
+                align: int = SHARD_ALIGN):
     """Views of this rank's rows of Wt [h][d] and of the packed codes (no copy)."""
     h, d = Wt.shape
-    lo, hi = shard_bounds(h, world, rank)
+    lo, hi = shard_bounds(h, world, rank, align)
     rb = code_bytes_per_row(d, n_m)
     if packed.numel() != h * rb:
         raise ValueError("packed codes size mismatch")
     return Wt[lo:hi], packed[lo * rb:hi * rb]
 
 
-def gather_columns(y_local: torch.Tensor, h: int, group=None) -> torch.Tensor:
+def gather_columns(y_local: torch.Tensor, h: int, group=None, align: int = SHARD_ALIGN) -> torch.Tensor:
     """All-gather the column slices y_g [B][hi_g - lo_g] of every rank into y [B][h]."""
     import torch.distributed as dist
     world = dist.get_world_size(group)
     B = y_local.shape[0]
-    width = max(shard_bounds(h, world, r)[1] - shard_bounds(h, world, r)[0] for r in range(world))
+    width = max(max(shard_bounds(h, world, r, align)[1] - shard_bounds(h, world, r, align)[0] for r in range(world)), 1)
     buf = torch.zeros((B, width), dtype=y_local.dtype, device=y_local.device)
     buf[:, :y_local.shape[1]] = y_local
     parts = [torch.empty((B, width), dtype=y_local.dtype, device=y_local.device) for _ in range(world)]
     dist.all_gather(parts, buf.contiguous(), group=group)        # NCCL over NVLink, or gloo on CPU
     cols = []
     for r in range(world):
-        lo, hi = shard_bounds(h, world, r)
+        lo, hi = shard_bounds(h, world, r, align)
         cols.append(parts[r][:, :hi - lo])
     return torch.cat(cols, dim=1)
 

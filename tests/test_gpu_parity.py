@@ -43,8 +43,9 @@ SHAPES = [  # (d, h, B) -- several tiles, ragged row tails, B up to the MMA grou
 @pytest.mark.parametrize("path", ["mma", "simt"])
 def test_bf16_shapes(n_m, d, h, B, path):
     inp = make_inputs(1000 + n_m * 7 + d + h + B, B=B, d=d, h=h, n_m=n_m, dtype="bf16")
-    if path == "mma" and d % 128:
-        # the MMA path tiles rows in 128-column code blocks (16 * n_m bytes): d % 128 == 0
+    if path == "mma" and (d % 128 or (n_m >= 4 and B > 4)):
+        # the MMA path tiles rows in 128-column code blocks (16 * n_m bytes): d % 128 == 0; with
+        # n_m >= 4 it serves one token group (B <= 4), larger batches go to the tcgen05 paths
         from paper_2506_23225_b200.mglu import MgluError, MGLU_ERR_UNSUPPORTED
         with pytest.raises(MgluError) as e:
             gpu_forward(inp, "bf16", n_m, "swish", path=path)
@@ -127,7 +128,7 @@ def test_one_hot_partials_bit_exact(n_m):
 def test_one_hot_forward_bit_exact(n_m, path):
     """Through the fused bf16 forward: Wt = 1, x one-hot at k, sigmoid g gives
     y[j] = (n_m - popcount(c[j,k])) / 2 exactly (each mask: bit 1 -> sigmoid(1)*0, bit 0 ->
-    sigmoid(0)*1).  Eight tokens per call, every k of d = 256 covered."""
+    sigmoid(0)*1).  Eight (or four) tokens per call, every k of d = 256 covered."""
     from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
     d, h = 256, 200
     inp = make_inputs(31 + n_m, B=1, d=d, h=h, n_m=n_m, dtype="bf16")
@@ -136,11 +137,12 @@ def test_one_hot_forward_bit_exact(n_m, path):
     Wt = torch.ones(h, d, device="cuda", dtype=torch.bfloat16)
     layer = Mglu(d, h, n_m, act="sigmoid", dtype="bf16", path=path)
     pop = bits.sum(axis=0)                                         # [h][d]
-    for k0 in range(0, d, 8):
-        x = torch.zeros(8, d, device="cuda", dtype=torch.bfloat16)
-        x[torch.arange(8), torch.arange(k0, k0 + 8)] = 1.0
+    T = 4 if (path == "mma" and n_m >= 4) else 8                   # (one MMA token group for n_m >= 4)
+    for k0 in range(0, d, T):
+        x = torch.zeros(T, d, device="cuda", dtype=torch.bfloat16)
+        x[torch.arange(T), torch.arange(k0, k0 + T)] = 1.0
         y = layer.forward(x, Wt, packed).float().cpu().numpy()
-        want = (n_m - pop[:, k0:k0 + 8].T) / 2.0
+        want = (n_m - pop[:, k0:k0 + T].T) / 2.0
         np.testing.assert_array_equal(y, want)
 
 

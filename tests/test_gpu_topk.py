@@ -74,6 +74,12 @@ def test_routed_forward_matches_oracle(path, n_m, K, B):
     rng = np.random.default_rng(K + B)
     G = topk_gate(rng.standard_normal((B, n_m)), K)
     layer = Mglu(d, h, n_m, act="swish", dtype="bf16", path=path)
+    if path == "mma" and n_m >= 4 and B > 4:         # one token group on the MMA path for n_m >= 4
+        from paper_2506_23225_b200.mglu import MGLU_ERR_UNSUPPORTED, MgluError
+        with pytest.raises(MgluError) as e:
+            layer.forward_routed(x, Wt, packed, torch.from_numpy(G.astype(np.float32)).cuda(), K)
+        assert e.value.status == MGLU_ERR_UNSUPPORTED
+        return
     y = layer.forward_routed(x, Wt, packed, torch.from_numpy(G.astype(np.float32)).cuda(), K)
     torch.cuda.synchronize()
     assert layer.last_path() == path

@@ -15,13 +15,20 @@ from paper_2506_23225_b200.shard import code_bytes_per_row, gather_columns, shar
 
 
 def test_shard_bounds_partition():
-    for h in (1, 7, 128, 14336, 28672, 11008):
-        for G in (1, 2, 3, 4, 8):
+    for h in (1, 7, 128, 300, 14336, 28672, 11008):
+        for G in (1, 2, 3, 4, 6, 8):
+            for align in (1, 8, 128):
+                b = [shard_bounds(h, G, r, align=align) for r in range(G)]
+                assert b[0][0] == 0 and b[-1][1] == h
+                assert all(b[r][1] == b[r + 1][0] for r in range(G - 1))
+                assert all(lo % align == 0 for lo, _ in b)          # shards start on a granule
+                sizes = [hi - lo for lo, hi in b]
+                assert max(sizes) - min(sizes) <= align
+    # default granule: whole 128-row tiles for every rank but possibly the last
+    for h in (11008, 14336, 28672):
+        for G in (3, 6, 8):
             b = [shard_bounds(h, G, r) for r in range(G)]
-            assert b[0][0] == 0 and b[-1][1] == h
-            assert all(b[r][1] == b[r + 1][0] for r in range(G - 1))
-            sizes = [hi - lo for lo, hi in b]
-            assert max(sizes) - min(sizes) <= 1
+            assert all((hi - lo) % 128 == 0 for lo, hi in b[:-1])
     # the BASELINE configs shard into whole 128-row tcgen05 tiles
     for h, G in ((14336, 8), (28672, 8), (28672, 4), (28672, 2)):
         assert all((hi - lo) % 128 == 0 for lo, hi in (shard_bounds(h, G, r) for r in range(G)))
@@ -36,12 +43,12 @@ def test_code_rows_are_pointer_offsets():
     rb = code_bytes_per_row(96, 4)
     for G in (2, 3):
         for r in range(G):
-            lo, hi = shard_bounds(10, G, r)
+            lo, hi = shard_bounds(10, G, r, align=1)
             np.testing.assert_array_equal(pack_np(inp["bits"][:, lo:hi]), full[lo * rb:hi * rb])
     Wt = torch.arange(10 * 96, dtype=torch.float32).reshape(10, 96)
     p = torch.from_numpy(full.copy())
-    W1, p1 = shard_layer(Wt, p, 4, 3, 1)
-    lo, hi = shard_bounds(10, 3, 1)
+    W1, p1 = shard_layer(Wt, p, 4, 3, 1, align=1)
+    lo, hi = shard_bounds(10, 3, 1, align=1)
     assert W1.data_ptr() == Wt[lo].data_ptr() and p1.data_ptr() == p[lo * rb].data_ptr()
 
 
@@ -57,7 +64,7 @@ def _worker(rank, world, port, out_dir):
     try:
         from oracle import COracle, decode_bf16
         from synth import make_inputs
-        d, h, n_m, B = 64, 37, 2, 3
+        d, h, n_m, B = 64, 300, 2, 3   # granules of 128 rows: a ragged last shard
         inp = make_inputs(11, B=B, d=d, h=h, n_m=n_m)
         o = COracle()
         packed = torch.from_numpy(o.pack(inp["bits"]))
@@ -93,7 +100,7 @@ def _ffn_worker(rank, world, port, out_dir):
         from oracle import ACT_SWISH, decode_bf16, dense_np, ffn_forward_np, mglu_forward_np
         from paper_2506_23225_b200.shard import shard_down
         from synth import make_inputs
-        d, h, n_m, B = 64, 45, 2, 2
+        d, h, n_m, B = 64, 300, 2, 2
         inp = make_inputs(21, B=B, d=d, h=h, n_m=n_m)
         x, Wt = decode_bf16(inp["x"]), decode_bf16(inp["Wt"])
         Wo = torch.from_numpy(np.random.default_rng(4).standard_normal((d, h)))

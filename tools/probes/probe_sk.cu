@@ -115,14 +115,13 @@ int main() {
            order, SB / 1024, S * SB / 1024, ms * 1e3 / K, bytes * K / (ms * 1e-3) / 1e9, l0);
     return 0;
   };
-  run(probe<128, 64>, 128, 64, 8, 0);
-  run(probe<128, 64>, 128, 64, 5, 0);
-  run(probe<128, 128>, 128, 128, 4, 0);
-  run(probe<128, 128>, 128, 128, 2, 0);
   run(probe<64, 256>, 64, 256, 4, 0);
-  run(probe<64, 128>, 64, 128, 8, 0);
   run(probe<32, 512>, 32, 512, 4, 0);
-  run(probe<128, 64>, 128, 64, 8, 1);
-  run(probe<128, 128>, 128, 128, 4, 1);
+  run(probe<16, 1024>, 16, 1024, 4, 0);
+  run(probe<8, 2048>, 8, 2048, 4, 0);
+  run(probe<8, 1024>, 8, 1024, 8, 0);
+  run(probe<8, 512>, 8, 512, 8, 0);
+  run(probe<64, 256>, 64, 256, 5, 0);
+  run(probe<8, 2048>, 8, 2048, 5, 0);
   return 0;
 }
