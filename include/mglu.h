@@ -186,6 +186,31 @@ mglu_status mglu_pack_logits_device(const float* logits, int n_m, int64_t h, int
 mglu_status mglu_unpack_masks_device(const uint8_t* packed, int n_m, int64_t h, int64_t d,
                                      uint8_t* bits, void* stream);
 
+/* Interop with per-element codes ("Combine the n_m binary masks into a single integer code
+ * per weight element"; Alg. 1's bit test `mask & (1 << (i-1))`; the listing's one uint8
+ * mask per element).  A code stream holds one w-bit field per
+ * element of the [h][d] layer, field (j, k) at bit offset w*(j*d + k), little-endian (bit b of the
+ * stream = bit b%8 of byte b/8); mask i is bit i-1 of the field.
+ *   w = n_m: the dense stream (h*d*n_m/8 bytes; n_m in {1,2,4,8,16});
+ *   w = 8:   one byte per element (the paper's listing; any n_m <= 8); w = 16: two bytes (n_m <= 16).
+ * Field bits at or above n_m must be zero (INVALID_ARG otherwise: "high-bit contamination",
+ * SPEC S:85).  mglu_codes_to_bits_host: stream -> 0/1 masks [n_m][h][d] (any d >= 1);
+ * mglu_pack_codes_host: stream -> this library's packed layout (d % 32 == 0 else UNSUPPORTED);
+ * mglu_unpack_codes_host: packed layout -> stream (the inverse; unused field bits written 0).
+ * Host memory, synchronous; streams are ceil(h*d*w/8) bytes. */
+size_t mglu_code_stream_bytes(int64_t d, int64_t h, int w);
+mglu_status mglu_codes_to_bits_host(const uint8_t* codes, int w, int n_m, int64_t h, int64_t d, uint8_t* bits);
+mglu_status mglu_pack_codes_host(const uint8_t* codes, int w, int n_m, int64_t h, int64_t d, uint8_t* packed);
+mglu_status mglu_unpack_codes_host(const uint8_t* packed, int n_m, int64_t h, int64_t d, int w, uint8_t* codes);
+
+/* Test hook ("injected mask-corruption flag"): with MGLU_DEBUG_FLIP_MASK_BIT set, every
+ * forward / partials call on the handle flips bit 0 of the caller's packed codes -- mask 1 of
+ * element (row 0, column 0) -- for the duration of the call (one XOR kernel before the forward and
+ * one after, stream-ordered; the buffer is restored when the call's work completes).  The parity
+ * suite must then fail at exactly that element.  0 clears the hook.  Not for production use. */
+#define MGLU_DEBUG_FLIP_MASK_BIT 1
+mglu_status mglu_set_debug(mglu_handle hd, int flags);
+
 /* Number of kernels the last mglu_forward on this handle enqueued (for launch accounting). */
 int mglu_last_launch_count(mglu_handle hd);
 

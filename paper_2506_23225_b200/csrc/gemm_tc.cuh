@@ -81,6 +81,7 @@ struct TcParams {
   int act;                   // g when the kernel is the kRuntimeAct instantiation
   int B, d, h;
   int stages;
+  float* z;                  // non-null: write Alg. 1's z [B][2 n_m][h] (s_i, t - s_i) instead of y
 };
 
 template <int NM, int ACT, int BN>
@@ -274,6 +275,14 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
 #pragma unroll
         for (int i = 0; i < MPC; ++i) {
           const float sg = 0.5f * (t + __uint_as_float(uv[i][q]));       // s_i = (t + u_i) / 2
+          if (p.z) {                                       // partials: this CTA's masks, no reduction
+            if (tq < p.B && m0 + m < p.h) {
+              float* zt = p.z + (size_t)tq * 2 * NM * p.h + m0 + m;
+              zt[(size_t)(moff + i) * p.h] = sg;
+              zt[(size_t)(NM + moff + i) * p.h] = t - sg;
+            }
+            continue;
+          }
           const float gate = (p.variant & 1) ? t : sg;                    // ablation variants
           const float value = (p.variant & 2) ? t : t - sg;
           const float wgt = p.G ? (tq < p.B ? p.G[(size_t)tq * NM + moff + i] : 0.f) : 1.f;   // routed (App. B)
@@ -281,6 +290,7 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
         }
         yp[ch][q] = acc;
       }
+      if (p.z) continue;
       if constexpr (NSPLIT > 1) {
         if (blockIdx.z == 1) {                             // partial of masks 5..8 -> rank 0's buffer
 #pragma unroll
@@ -302,7 +312,7 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
     cluster_arrive();                                      // partials delivered (release / acquire)
     cluster_wait();
   }
-  if (NSPLIT > 1 && warp < kTcMaskWarps && blockIdx.z == 0) {
+  if (NSPLIT > 1 && warp < kTcMaskWarps && blockIdx.z == 0 && !p.z) {
     const int g = warp >> 2;
     const int m = (warp & 3) * 32 + lane;
     const int grow = m0 + m;

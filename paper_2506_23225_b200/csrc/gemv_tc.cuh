@@ -69,6 +69,7 @@ struct SkParams {
   uint32_t* flags;      // [gridDim.x], 0 between calls
   int B, d, h, act;
   int upt;              // units per tile = ceil(d / KS)
+  float* z;             // non-null: write Alg. 1's z [B][2 n_m][h] (s_i, t - s_i) instead of y
   int units_base, units_rem;   // CTA c owns units_base + (c < units_rem) units
   int stages;
 };
@@ -350,7 +351,16 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
 #pragma unroll
           for (int q = 0; q < CH; ++q) {
             const int tok = ch * CH + q;
-            if (tok < B) {
+            if (tok < B && p.z) {                          // partials (debug / parity of a5, a6)
+              const float t = f[0][q];
+              float* zt = p.z + (size_t)tok * 2 * NM * p.h + grow;
+#pragma unroll
+              for (int i = 0; i < NM; ++i) {
+                const float sg = 0.5f * (t + f[1 + i][q]);
+                zt[(size_t)i * p.h] = sg;
+                zt[(size_t)(NM + i) * p.h] = t - sg;
+              }
+            } else if (tok < B) {
               const float t = f[0][q];
               float y = 0.f;
 #pragma unroll

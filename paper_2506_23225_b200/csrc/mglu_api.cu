@@ -31,6 +31,7 @@ struct mglu_ctx {
   int n_m = 0, act = 0, dtype = 0, device = 0;
   int path = MGLU_PATH_AUTO;
   int variant = 0;           // partial-mask ablation variant (mglu_set_variant)
+  int debug = 0;             // test hooks (mglu_set_debug)
   int last_path = 0, last_launches = 0;
   int num_sms = 148;
   int max_smem_optin = 0;
@@ -61,10 +62,13 @@ struct mglu_ctx {
 
 namespace {
 
-// gate weights of the routed forward being enqueued by this host thread (nullptr: plain forward);
-// set and cleared by mglu_forward_routed around the regular dispatch
-thread_local const float* t_routed_G = nullptr;
-thread_local int t_routed_K = 0;   // K of the routed call (0: unknown -> every mask evaluated)
+// per-call arguments beyond (x, B, Wt, codes, out) that reach every launcher
+struct Call {
+  cudaStream_t st;
+  const float* G = nullptr;   // routed gate weights [B][n_m] (mglu_forward_routed), nullptr: Eq. 3
+  int K = 0;                  // K of the routed call (0: unknown -> every mask evaluated)
+  float* z = nullptr;         // mglu_forward_partials: Alg. 1's z [B][2 n_m][h] instead of y
+};
 
 const char* kStatusStr[] = {"MGLU_OK", "MGLU_ERR_INVALID_ARG", "MGLU_ERR_UNSUPPORTED",
                             "MGLU_ERR_MISALIGNED", "MGLU_ERR_CUDA", "MGLU_ERR_OOM"};
@@ -113,41 +117,41 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // ------------------------------------------------------------------ SIMT dispatch
 template <typename T, int NM, int ACT, bool PARTIALS>
 cudaError_t run_simt(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
-                     void* out, float* z, cudaStream_t st) {
+                     void* out, float* z, const Call& cl) {
   const int warps_per_block = 8;
   int64_t blocks = (hd->h + warps_per_block - 1) / warps_per_block;
   const int64_t cap = (int64_t)hd->num_sms * 8;
   if (blocks > cap) blocks = cap;
   return launch_pdl(mglu::gemv_simt_kernel<T, NM, ACT, PARTIALS>, dim3((unsigned)blocks),
-                    dim3(warps_per_block * 32), 0, st, (const T*)x, B, (int)hd->d, (const T*)Wt,
-                    (const uint8_t*)codes, (int)hd->h, (T*)out, z, t_routed_G, hd->variant, hd->act);
+                    dim3(warps_per_block * 32), 0, cl.st, (const T*)x, B, (int)hd->d, (const T*)Wt,
+                    (const uint8_t*)codes, (int)hd->h, (T*)out, z, cl.G, hd->variant, hd->act);
 }
 
 template <typename T, bool PARTIALS, int NM>
 cudaError_t simt_act(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
-                     void* out, float* z, cudaStream_t st) {
+                     void* out, float* z, const Call& cl) {
   switch (hd->act) {
-    case MGLU_ACT_SWISH: return run_simt<T, NM, mglu::kSwish, PARTIALS>(hd, x, B, Wt, codes, out, z, st);
-    default: return run_simt<T, NM, mglu::kRuntimeAct, PARTIALS>(hd, x, B, Wt, codes, out, z, st);   // g at runtime
+    case MGLU_ACT_SWISH: return run_simt<T, NM, mglu::kSwish, PARTIALS>(hd, x, B, Wt, codes, out, z, cl);
+    default: return run_simt<T, NM, mglu::kRuntimeAct, PARTIALS>(hd, x, B, Wt, codes, out, z, cl);   // g at runtime
   }
 }
 
 template <typename T, bool PARTIALS>
 cudaError_t simt_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
-                    void* out, float* z, cudaStream_t st) {
+                    void* out, float* z, const Call& cl) {
 #ifdef MGLU_DEC_ONLY
   return cudaErrorInvalidValue;
 #endif
   switch (hd->n_m) {
-    case 1: return simt_act<T, PARTIALS, 1>(hd, x, B, Wt, codes, out, z, st);
-    case 2: return simt_act<T, PARTIALS, 2>(hd, x, B, Wt, codes, out, z, st);
-    case 3: return simt_act<T, PARTIALS, 3>(hd, x, B, Wt, codes, out, z, st);
-    case 4: return simt_act<T, PARTIALS, 4>(hd, x, B, Wt, codes, out, z, st);
-    case 5: return simt_act<T, PARTIALS, 5>(hd, x, B, Wt, codes, out, z, st);
-    case 6: return simt_act<T, PARTIALS, 6>(hd, x, B, Wt, codes, out, z, st);
-    case 7: return simt_act<T, PARTIALS, 7>(hd, x, B, Wt, codes, out, z, st);
-    case 8: return simt_act<T, PARTIALS, 8>(hd, x, B, Wt, codes, out, z, st);
-    case 16: return simt_act<T, PARTIALS, 16>(hd, x, B, Wt, codes, out, z, st);
+    case 1: return simt_act<T, PARTIALS, 1>(hd, x, B, Wt, codes, out, z, cl);
+    case 2: return simt_act<T, PARTIALS, 2>(hd, x, B, Wt, codes, out, z, cl);
+    case 3: return simt_act<T, PARTIALS, 3>(hd, x, B, Wt, codes, out, z, cl);
+    case 4: return simt_act<T, PARTIALS, 4>(hd, x, B, Wt, codes, out, z, cl);
+    case 5: return simt_act<T, PARTIALS, 5>(hd, x, B, Wt, codes, out, z, cl);
+    case 6: return simt_act<T, PARTIALS, 6>(hd, x, B, Wt, codes, out, z, cl);
+    case 7: return simt_act<T, PARTIALS, 7>(hd, x, B, Wt, codes, out, z, cl);
+    case 8: return simt_act<T, PARTIALS, 8>(hd, x, B, Wt, codes, out, z, cl);
+    case 16: return simt_act<T, PARTIALS, 16>(hd, x, B, Wt, codes, out, z, cl);
     default: return cudaErrorInvalidValue;                  // (n_m = 0 dense handles never get here)
   }
 }
@@ -254,11 +258,12 @@ int dec_l2pf() {
 
 template <int NM, int ACT, int NB, int KSEL>
 cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
-                       void* out, cudaStream_t st) {
+                       void* out, const Call& cl) {
   mglu::DecParams p;
   p.x = (const __nv_bfloat16*)x;
   p.out = (__nv_bfloat16*)out;
-  p.G = t_routed_G;
+  p.G = cl.G;
+  p.z = cl.z;
   p.variant = hd->variant;
   p.act = hd->act;
   p.B = B;
@@ -300,53 +305,53 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   auto kern = mglu::gemv_mma_kernel<NM, ACT, NB, KSEL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(kern, dim3((unsigned)ncta), dim3(mglu::kDecThreads), smem, st, p, maps);
+  return launch_pdl(kern, dim3((unsigned)ncta), dim3(mglu::kDecThreads), smem, cl.st, p, maps);
 }
 
 template <int NM, int ACT>
 cudaError_t run_mma(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
-                    void* out, cudaStream_t st) {
+                    void* out, const Call& cl) {
   // routed (Top-K) swish forward: evaluate only the masks some token selected -- at most K per
   // token, so min(n_m, B*K) slots, rounded up to a power of two (other activations and larger
   // unions run all masks with the weights in the epilogue)
   if constexpr (ACT == mglu::kSwish && NM >= 2) {
     // (B > 4: B*K >= 5 tokens' selections cover min(n_m, 5) >= every slot count below -- all masks)
-    if (t_routed_G && t_routed_K > 0 && hd->variant == 0 && B <= 4) {
-      const int u = std::min(NM, B * t_routed_K);
-      if (u <= 1) return run_mma_nb<NM, ACT, 1, 1>(hd, x, B, Wt, codes, out, st);
-      if (u <= 2 && NM > 2) return run_mma_nb<NM, ACT, 1, 2>(hd, x, B, Wt, codes, out, st);
+    if (cl.G && cl.K > 0 && hd->variant == 0 && B <= 4) {
+      const int u = std::min(NM, B * cl.K);
+      if (u <= 1) return run_mma_nb<NM, ACT, 1, 1>(hd, x, B, Wt, codes, out, cl);
+      if (u <= 2 && NM > 2) return run_mma_nb<NM, ACT, 1, 2>(hd, x, B, Wt, codes, out, cl);
       if constexpr (NM == 8)
-        if (u <= 4) return run_mma_nb<NM, ACT, 1, 4>(hd, x, B, Wt, codes, out, st);
+        if (u <= 4) return run_mma_nb<NM, ACT, 1, 4>(hd, x, B, Wt, codes, out, cl);
     }
   }
-  if constexpr (NM >= 4) return B <= 4 ? run_mma_nb<NM, ACT, 1, 0>(hd, x, B, Wt, codes, out, st) : cudaErrorInvalidValue;
-  else return B <= 4 ? run_mma_nb<NM, ACT, 1, 0>(hd, x, B, Wt, codes, out, st)
-                     : run_mma_nb<NM, ACT, 2, 0>(hd, x, B, Wt, codes, out, st);
+  if constexpr (NM >= 4) return B <= 4 ? run_mma_nb<NM, ACT, 1, 0>(hd, x, B, Wt, codes, out, cl) : cudaErrorInvalidValue;
+  else return B <= 4 ? run_mma_nb<NM, ACT, 1, 0>(hd, x, B, Wt, codes, out, cl)
+                     : run_mma_nb<NM, ACT, 2, 0>(hd, x, B, Wt, codes, out, cl);
 }
 
 template <int NM>
 cudaError_t mma_act(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes, void* out,
-                    cudaStream_t st) {
+                    const Call& cl) {
   switch (hd->act) {
-    case MGLU_ACT_SWISH: return run_mma<NM, mglu::kSwish>(hd, x, B, Wt, codes, out, st);
-    default: return run_mma<NM, mglu::kRuntimeAct>(hd, x, B, Wt, codes, out, st);   // g at runtime
+    case MGLU_ACT_SWISH: return run_mma<NM, mglu::kSwish>(hd, x, B, Wt, codes, out, cl);
+    default: return run_mma<NM, mglu::kRuntimeAct>(hd, x, B, Wt, codes, out, cl);   // g at runtime
   }
 }
 
 cudaError_t mma_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes, void* out,
-                   cudaStream_t st) {
+                   const Call& cl) {
 #ifdef MGLU_DEC_ONLY   // experiment build (tools): the n_m in {1, 4} Swish decode kernels only
-  if (hd->act != MGLU_ACT_SWISH || B > 4 || t_routed_G) return cudaErrorInvalidValue;
-  if (hd->n_m == 4) return run_mma_nb<4, mglu::kSwish, 1, 0>(hd, x, B, Wt, codes, out, st);
-  if (hd->n_m == 1) return run_mma_nb<1, mglu::kSwish, 1, 0>(hd, x, B, Wt, codes, out, st);
+  if (hd->act != MGLU_ACT_SWISH || B > 4 || cl.G) return cudaErrorInvalidValue;
+  if (hd->n_m == 4) return run_mma_nb<4, mglu::kSwish, 1, 0>(hd, x, B, Wt, codes, out, cl);
+  if (hd->n_m == 1) return run_mma_nb<1, mglu::kSwish, 1, 0>(hd, x, B, Wt, codes, out, cl);
   return cudaErrorInvalidValue;
 #endif
   switch (hd->n_m) {
-    case 0: return run_mma<0, mglu::kIdentity>(hd, x, B, Wt, codes, out, st);   // dense projection
-    case 1: return mma_act<1>(hd, x, B, Wt, codes, out, st);
-    case 2: return mma_act<2>(hd, x, B, Wt, codes, out, st);
-    case 4: return mma_act<4>(hd, x, B, Wt, codes, out, st);
-    default: return mma_act<8>(hd, x, B, Wt, codes, out, st);
+    case 0: return run_mma<0, mglu::kIdentity>(hd, x, B, Wt, codes, out, cl);   // dense projection
+    case 1: return mma_act<1>(hd, x, B, Wt, codes, out, cl);
+    case 2: return mma_act<2>(hd, x, B, Wt, codes, out, cl);
+    case 4: return mma_act<4>(hd, x, B, Wt, codes, out, cl);
+    default: return mma_act<8>(hd, x, B, Wt, codes, out, cl);
   }
 }
 
@@ -397,7 +402,7 @@ bool encode_2d_u32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t row
 
 template <int NM, int ACT, int BN>
 cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
-                      cudaStream_t st) {
+                      const Call& cl) {
   CUtensorMap mX, mW, mC;
   const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
   if (!encode_2d_bf16(&mX, x, hd->d, B, mglu::kTcK, BN, sw) ||
@@ -407,7 +412,8 @@ cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
     return cudaErrorInvalidValue;
   mglu::TcParams p;
   p.out = (__nv_bfloat16*)out;
-  p.G = t_routed_G;
+  p.G = cl.G;
+  p.z = cl.z;
   p.variant = hd->variant;
   p.act = hd->act;
   p.B = (int)B;
@@ -429,7 +435,7 @@ cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   cfg.gridDim = grid;
   cfg.blockDim = dim3(mglu::kTcThreads);
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
+  cfg.stream = cl.st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
@@ -446,32 +452,32 @@ cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
 // B and the kernel streams W and the mask words at HBM rate); large batches the TMEM-limited tile
 template <int NM, int ACT>
 cudaError_t run_tc(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
-                   cudaStream_t st) {
-  if (B <= 16) return run_tc_bn<NM, ACT, 16>(hd, x, B, Wt, codes, out, st);
-  if (B <= 32) return run_tc_bn<NM, ACT, 32>(hd, x, B, Wt, codes, out, st);
-  if (B <= 64 || mglu::TcCfg<NM>::BN == 64) return run_tc_bn<NM, ACT, 64>(hd, x, B, Wt, codes, out, st);
-  return run_tc_bn<NM, ACT, mglu::TcCfg<NM>::BN>(hd, x, B, Wt, codes, out, st);
+                   const Call& cl) {
+  if (B <= 16) return run_tc_bn<NM, ACT, 16>(hd, x, B, Wt, codes, out, cl);
+  if (B <= 32) return run_tc_bn<NM, ACT, 32>(hd, x, B, Wt, codes, out, cl);
+  if (B <= 64 || mglu::TcCfg<NM>::BN == 64) return run_tc_bn<NM, ACT, 64>(hd, x, B, Wt, codes, out, cl);
+  return run_tc_bn<NM, ACT, mglu::TcCfg<NM>::BN>(hd, x, B, Wt, codes, out, cl);
 }
 
 template <int NM>
 cudaError_t tc_act(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
-                   cudaStream_t st) {
+                   const Call& cl) {
   switch (hd->act) {
-    case MGLU_ACT_SWISH: return run_tc<NM, mglu::kSwish>(hd, x, B, Wt, codes, out, st);
-    default: return run_tc<NM, mglu::kRuntimeAct>(hd, x, B, Wt, codes, out, st);   // g at runtime
+    case MGLU_ACT_SWISH: return run_tc<NM, mglu::kSwish>(hd, x, B, Wt, codes, out, cl);
+    default: return run_tc<NM, mglu::kRuntimeAct>(hd, x, B, Wt, codes, out, cl);   // g at runtime
   }
 }
 
 cudaError_t tc_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
-                  cudaStream_t st) {
+                  const Call& cl) {
 #ifdef MGLU_DEC_ONLY
   return cudaErrorInvalidValue;
 #endif
   switch (hd->n_m) {
-    case 1: return tc_act<1>(hd, x, B, Wt, codes, out, st);
-    case 2: return tc_act<2>(hd, x, B, Wt, codes, out, st);
-    case 4: return tc_act<4>(hd, x, B, Wt, codes, out, st);
-    default: return tc_act<8>(hd, x, B, Wt, codes, out, st);
+    case 1: return tc_act<1>(hd, x, B, Wt, codes, out, cl);
+    case 2: return tc_act<2>(hd, x, B, Wt, codes, out, cl);
+    case 4: return tc_act<4>(hd, x, B, Wt, codes, out, cl);
+    default: return tc_act<8>(hd, x, B, Wt, codes, out, cl);
   }
 }
 
@@ -503,7 +509,7 @@ cudaError_t sk_alloc(mglu_ctx* hd) {
 
 template <int NM, int BN, int MG>
 cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
-                      cudaStream_t st) {
+                      const Call& cl) {
   using C = mglu::SkCfg<NM, BN, MG>;
   CUtensorMap mW, mX, mC;
   const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
@@ -514,7 +520,8 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
     return cudaErrorInvalidValue;
   mglu::SkParams p;
   p.out = (__nv_bfloat16*)out;
-  p.G = t_routed_G;
+  p.G = cl.G;
+  p.z = cl.z;
   p.variant = hd->variant;
   p.B = (int)B;
   p.d = (int)hd->d;
@@ -537,36 +544,36 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   auto kern = mglu::gemv_tc_kernel<NM, BN, MG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(kern, dim3((unsigned)G), dim3(C::THREADS), smem, st, p, mW, mX, mC);
+  return launch_pdl(kern, dim3((unsigned)G), dim3(C::THREADS), smem, cl.st, p, mW, mX, mC);
 }
 
 // two masker groups when the TMEM budget allows, else one
 template <int NM, int BN>
 cudaError_t run_sk_mg(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
-                      cudaStream_t st) {
-  if constexpr (mglu::SkCfg<NM, BN, 2>::ok) return run_sk_bn<NM, BN, 2>(hd, x, B, Wt, codes, out, st);
-  else return run_sk_bn<NM, BN, 1>(hd, x, B, Wt, codes, out, st);
+                      const Call& cl) {
+  if constexpr (mglu::SkCfg<NM, BN, 2>::ok) return run_sk_bn<NM, BN, 2>(hd, x, B, Wt, codes, out, cl);
+  else return run_sk_bn<NM, BN, 1>(hd, x, B, Wt, codes, out, cl);
 }
 
 template <int NM>
 cudaError_t run_sk(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
-                   cudaStream_t st) {
-  if (B <= 16) return run_sk_mg<NM, 16>(hd, x, B, Wt, codes, out, st);
-  if (B <= 32) return run_sk_mg<NM, 32>(hd, x, B, Wt, codes, out, st);
-  if constexpr (NM < 8) return run_sk_mg<NM, 64>(hd, x, B, Wt, codes, out, st);
+                   const Call& cl) {
+  if (B <= 16) return run_sk_mg<NM, 16>(hd, x, B, Wt, codes, out, cl);
+  if (B <= 32) return run_sk_mg<NM, 32>(hd, x, B, Wt, codes, out, cl);
+  if constexpr (NM < 8) return run_sk_mg<NM, 64>(hd, x, B, Wt, codes, out, cl);
   return cudaErrorInvalidValue;
 }
 
 cudaError_t sk_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
-                  cudaStream_t st) {
+                  const Call& cl) {
 #ifdef MGLU_DEC_ONLY
   return cudaErrorInvalidValue;
 #endif
   switch (hd->n_m) {
-    case 1: return run_sk<1>(hd, x, B, Wt, codes, out, st);
-    case 2: return run_sk<2>(hd, x, B, Wt, codes, out, st);
-    case 4: return run_sk<4>(hd, x, B, Wt, codes, out, st);
-    default: return run_sk<8>(hd, x, B, Wt, codes, out, st);
+    case 1: return run_sk<1>(hd, x, B, Wt, codes, out, cl);
+    case 2: return run_sk<2>(hd, x, B, Wt, codes, out, cl);
+    case 4: return run_sk<4>(hd, x, B, Wt, codes, out, cl);
+    default: return run_sk<8>(hd, x, B, Wt, codes, out, cl);
   }
 }
 
@@ -695,6 +702,13 @@ mglu_status mglu_set_variant(mglu_handle hd, int variant) {
   return MGLU_OK;
 }
 
+mglu_status mglu_set_debug(mglu_handle hd, int flags) {
+  if (!hd || (flags & ~MGLU_DEBUG_FLIP_MASK_BIT)) return MGLU_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> g(hd->mu);
+  hd->debug = flags;
+  return MGLU_OK;
+}
+
 int mglu_last_launch_count(mglu_handle hd) { return hd ? hd->last_launches : -1; }
 int mglu_last_path(mglu_handle hd) { return hd ? hd->last_path : -1; }
 
@@ -702,9 +716,12 @@ int mglu_last_path(mglu_handle hd) { return hd ? hd->last_path : -1; }
 
 // the forward on an explicit path (AUTO resolved here); shared by mglu_forward and
 // mglu_forward_routed
+// test hook: flip one bit of the caller's packed codes (mglu_set_debug)
+__global__ void flip_bit_kernel(uint8_t* p, uint8_t m) { p[0] ^= m; }
+
 static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, const void* Wt,
-                                   const void* packed, void* out, void* stream, int path) {
-  mglu_status s = check_ptrs(hd, x, B, Wt, packed, out);
+                                   const void* packed, void* out, int path, const Call& cl) {
+  mglu_status s = check_ptrs(hd, x, B, Wt, packed, cl.z ? (const void*)cl.z : out);
   if (s != MGLU_OK) return s;
   hd->last_launches = 0;
   if (B == 0) return MGLU_OK;
@@ -735,22 +752,23 @@ static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, con
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != hd->device) cudaSetDevice(hd->device);
-  cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
   int launches = 0;
+  const bool fault = (hd->debug & MGLU_DEBUG_FLIP_MASK_BIT) && packed && hd->n_m > 0;
+  if (fault) flip_bit_kernel<<<1, 1, 0, cl.st>>>((uint8_t*)const_cast<void*>(packed), 1);
   if (path == MGLU_PATH_MMA) {
     if (!mma_can_serve(hd, B)) {
       if (prev != hd->device) cudaSetDevice(prev);
       return set_err(hd, MGLU_ERR_UNSUPPORTED, "MMA path needs bf16, 1 <= B <= 8 (B <= 4 for n_m >= 4), d % 128 == 0");
     }
-    e = mma_nm(hd, x, (int)B, Wt, packed, out, st);
+    e = mma_nm(hd, x, (int)B, Wt, packed, out, cl);
     launches = 1;
   } else if (path == MGLU_PATH_TCGEN05) {
     if (!tc_can_serve(hd, B)) {
       if (prev != hd->device) cudaSetDevice(prev);
       return set_err(hd, MGLU_ERR_UNSUPPORTED, "tcgen05 path needs bf16 and d * n_m % 128 == 0");
     }
-    e = tc_nm(hd, x, B, Wt, packed, out, st);
+    e = tc_nm(hd, x, B, Wt, packed, out, cl);
     launches = 1;
   } else if (path == MGLU_PATH_TCDEC) {
     if (!sk_can_serve(hd, B)) {
@@ -758,14 +776,18 @@ static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, con
       return set_err(hd, MGLU_ERR_UNSUPPORTED,
                      "tcgen05 decode path needs bf16, 1 <= B <= 64 (32 for n_m = 8), d % 64 == 0, d * n_m % 128 == 0");
     }
-    e = sk_nm(hd, x, B, Wt, packed, out, st);
+    e = sk_nm(hd, x, B, Wt, packed, out, cl);
     launches = 1;
   } else {
-    e = hd->dtype == MGLU_BF16
-            ? simt_nm<__nv_bfloat16, false>(hd, x, (int)B, Wt, packed, out, nullptr, st)
-            : simt_nm<float, false>(hd, x, (int)B, Wt, packed, out, nullptr, st);
+    if (cl.z)
+      e = hd->dtype == MGLU_BF16 ? simt_nm<__nv_bfloat16, true>(hd, x, (int)B, Wt, packed, nullptr, cl.z, cl)
+                                 : simt_nm<float, true>(hd, x, (int)B, Wt, packed, nullptr, cl.z, cl);
+    else
+      e = hd->dtype == MGLU_BF16 ? simt_nm<__nv_bfloat16, false>(hd, x, (int)B, Wt, packed, out, nullptr, cl)
+                                 : simt_nm<float, false>(hd, x, (int)B, Wt, packed, out, nullptr, cl);
     launches = 1;
   }
+  if (fault) flip_bit_kernel<<<1, 1, 0, cl.st>>>((uint8_t*)const_cast<void*>(packed), 1);
   if (prev != hd->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_fail(hd, e, "mglu_forward launch");
   hd->last_path = path;
@@ -783,7 +805,9 @@ mglu_status mglu_forward(mglu_handle hd, const void* x, int64_t B, const void* W
     std::lock_guard<std::mutex> g(hd->mu);
     path = hd->path;
   }
-  return forward_on_path(hd, x, B, Wt, packed, out, stream, path);
+  Call cl;
+  cl.st = (cudaStream_t)stream;
+  return forward_on_path(hd, x, B, Wt, packed, out, path, cl);
 }
 
 mglu_status mglu_router_topk(mglu_handle hd, const void* x, int64_t B, const void* Wr, int K, float* G,
@@ -828,36 +852,33 @@ mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const 
     std::lock_guard<std::mutex> g(hd->mu);
     path = hd->path;
   }
-  // the routed weights reach every launcher through a thread-local pointer; the MMA path also skips
-  // the masks no token selected, the tensor-core paths weigh every mask in their epilogues
+  // the routed weights reach every launcher in the call arguments; the MMA path also skips the
+  // masks no token selected, the tensor-core paths weigh every mask in their epilogues
   if (path == MGLU_PATH_AUTO && K > 0 && mma_can_serve(hd, B)) path = MGLU_PATH_MMA;   // it skips masks
-  t_routed_G = G;
-  t_routed_K = K;
-  s = forward_on_path(hd, x, B, Wt, packed, out, stream, path);
-  t_routed_G = nullptr;
-  t_routed_K = 0;
-  return s;
+  Call cl;
+  cl.st = (cudaStream_t)stream;
+  cl.G = G;
+  cl.K = K;
+  return forward_on_path(hd, x, B, Wt, packed, out, path, cl);
 }
 
 mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, const void* Wt,
                                   const void* packed, float* z, void* stream) {
-  if (hd && hd->n_m == 0) return set_err(hd, MGLU_ERR_UNSUPPORTED, "partials need masks (n_m >= 1)");
-  mglu_status s = check_ptrs(hd, x, B, Wt, packed, z);
-  if (s != MGLU_OK) return s;
-  hd->last_launches = 0;
-  if (B == 0) return MGLU_OK;
-  int prev = 0;
-  cudaGetDevice(&prev);
-  if (prev != hd->device) cudaSetDevice(hd->device);
-  cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = hd->dtype == MGLU_BF16
-                      ? simt_nm<__nv_bfloat16, true>(hd, x, (int)B, Wt, packed, nullptr, z, st)
-                      : simt_nm<float, true>(hd, x, (int)B, Wt, packed, nullptr, z, st);
-  if (prev != hd->device) cudaSetDevice(prev);
-  if (e != cudaSuccess) return cuda_fail(hd, e, "mglu_forward_partials launch");
-  hd->last_path = MGLU_PATH_SIMT;
-  hd->last_launches = 1;
-  return MGLU_OK;
+  if (!hd) return MGLU_ERR_INVALID_ARG;
+  if (hd->n_m == 0) return set_err(hd, MGLU_ERR_UNSUPPORTED, "partials need masks (n_m >= 1)");
+  if (!z) return set_err(hd, MGLU_ERR_INVALID_ARG, "null z");
+  int path;
+  {
+    std::lock_guard<std::mutex> g(hd->mu);
+    path = hd->path;
+  }
+  // AUTO: the SIMT kernel (Alg. 1 as written); an explicit path: that kernel, whose epilogue writes
+  // s_i and t - s_i instead of y (each fast path's own value streams, for the parity tests)
+  if (path == MGLU_PATH_AUTO) path = MGLU_PATH_SIMT;
+  Call cl;
+  cl.st = (cudaStream_t)stream;
+  cl.z = z;
+  return forward_on_path(hd, x, B, Wt, packed, nullptr, path, cl);
 }
 
 mglu_status mglu_forward_host(mglu_handle hd, const void* x_host, int64_t B, const void* Wt,
@@ -930,6 +951,63 @@ mglu_status mglu_unpack_masks_host(const uint8_t* packed, int n_m, int64_t h, in
         const uint32_t w = get_le32(packed + ((j * groups + k / 32) * n_m + i) * 4);
         bits[i * hd + j * d + k] = (uint8_t)((w >> mglu::code_bit_of((int)(k % 32))) & 1u);
       }
+  return MGLU_OK;
+}
+
+// ------------------------------------------------------------------ per-element code streams
+static bool valid_code_width(int w, int n_m) {
+  return (w == 1 || w == 2 || w == 4 || w == 8 || w == 16) && n_m >= 1 && n_m <= w && valid_nm(n_m);
+}
+// field (element e) of a w-bit little-endian stream; w divides 8 or is 16, so a field never
+// straddles a byte boundary except for w = 16 (two whole bytes)
+static uint32_t code_field(const uint8_t* c, int w, int64_t e) {
+  if (w == 16) return (uint32_t)c[2 * e] | ((uint32_t)c[2 * e + 1] << 8);
+  const int64_t bit = e * w;
+  return (c[bit >> 3] >> (bit & 7)) & ((1u << w) - 1u);
+}
+
+size_t mglu_code_stream_bytes(int64_t d, int64_t h, int w) {
+  if (d < 0 || h < 0 || !(w == 1 || w == 2 || w == 4 || w == 8 || w == 16)) return 0;
+  return (size_t)((h * d * w + 7) / 8);
+}
+
+mglu_status mglu_codes_to_bits_host(const uint8_t* codes, int w, int n_m, int64_t h, int64_t d, uint8_t* bits) {
+  if (!codes || !bits || h < 0 || d < 0) return MGLU_ERR_INVALID_ARG;
+  if (!valid_code_width(w, n_m)) return MGLU_ERR_UNSUPPORTED;
+  const int64_t hd = h * d;
+  for (int64_t e = 0; e < hd; ++e)
+    if (code_field(codes, w, e) >> n_m) return MGLU_ERR_INVALID_ARG;      // high-bit contamination
+  for (int64_t e = 0; e < hd; ++e) {
+    const uint32_t f = code_field(codes, w, e);
+    for (int i = 0; i < n_m; ++i) bits[i * hd + e] = (uint8_t)((f >> i) & 1u);   // mask i+1 = bit i
+  }
+  return MGLU_OK;
+}
+
+mglu_status mglu_pack_codes_host(const uint8_t* codes, int w, int n_m, int64_t h, int64_t d, uint8_t* packed) {
+  if (!codes || !packed || h < 0 || d < 0) return MGLU_ERR_INVALID_ARG;
+  if (!valid_code_width(w, n_m) || d % 32) return MGLU_ERR_UNSUPPORTED;
+  const int64_t hd = h * d;
+  for (int64_t e = 0; e < hd; ++e)
+    if (code_field(codes, w, e) >> n_m) return MGLU_ERR_INVALID_ARG;
+  pack_words(n_m, h, d, packed, [&](int i, int64_t j, int64_t k) { return (code_field(codes, w, j * d + k) >> i) & 1u; });
+  return MGLU_OK;
+}
+
+mglu_status mglu_unpack_codes_host(const uint8_t* packed, int n_m, int64_t h, int64_t d, int w, uint8_t* codes) {
+  if (!codes || !packed || h < 0 || d < 0) return MGLU_ERR_INVALID_ARG;
+  if (!valid_code_width(w, n_m) || d % 32) return MGLU_ERR_UNSUPPORTED;
+  const int64_t groups = d / 32;
+  memset(codes, 0, mglu_code_stream_bytes(d, h, w));
+  for (int64_t j = 0; j < h; ++j)
+    for (int64_t k = 0; k < d; ++k) {
+      uint32_t f = 0;
+      for (int i = 0; i < n_m; ++i)
+        f |= ((get_le32(packed + ((j * groups + k / 32) * n_m + i) * 4) >> mglu::code_bit_of((int)(k % 32))) & 1u) << i;
+      const int64_t e = j * d + k;
+      if (w == 16) { codes[2 * e] = (uint8_t)f; codes[2 * e + 1] = (uint8_t)(f >> 8); }
+      else codes[(e * w) >> 3] |= (uint8_t)(f << ((e * w) & 7));
+    }
   return MGLU_OK;
 }
 

@@ -61,6 +61,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "mglu_destroy": ([vp], c_int),
         "mglu_set_path": ([vp, c_int], c_int),
         "mglu_set_variant": ([vp, c_int], c_int),
+        "mglu_set_debug": ([vp, c_int], c_int),
         "mglu_forward": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_forward_partials": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_forward_host": ([vp, vp, i64, vp, vp, vp, vp], c_int),
@@ -68,6 +69,10 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "mglu_forward_routed": ([vp, vp, i64, vp, vp, vp, c_int, vp, vp], c_int),
         "mglu_packed_mask_bytes": ([i64, i64, c_int], sz),
         "mglu_pack_masks_host": ([vp, c_int, i64, i64, vp], c_int),
+        "mglu_code_stream_bytes": ([i64, i64, c_int], sz),
+        "mglu_codes_to_bits_host": ([vp, c_int, c_int, i64, i64, vp], c_int),
+        "mglu_pack_codes_host": ([vp, c_int, c_int, i64, i64, vp], c_int),
+        "mglu_unpack_codes_host": ([vp, c_int, i64, i64, c_int, vp], c_int),
         "mglu_pack_logits_host": ([vp, c_int, i64, i64, vp], c_int),
         "mglu_unpack_masks_host": ([vp, c_int, i64, i64, vp], c_int),
         "mglu_pack_masks_device": ([vp, c_int, i64, i64, vp, vp], c_int),
@@ -199,6 +204,37 @@ def mglu_unpack_masks_host(packed: np.ndarray, n_m: int, h: int, d: int) -> np.n
     return out
 
 
+def mglu_code_stream_bytes(d: int, h: int, w: int) -> int:
+    return int(load_library().mglu_code_stream_bytes(d, h, w))
+
+
+def mglu_codes_to_bits_host(codes: np.ndarray, w: int, n_m: int, h: int, d: int) -> np.ndarray:
+    """Per-element code stream (w-bit fields, mask i = bit i-1) -> 0/1 masks [n_m][h][d]."""
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    if codes.size != mglu_code_stream_bytes(d, h, w):
+        raise MgluError(MGLU_ERR_INVALID_ARG, "code stream size mismatch")
+    out = np.empty((n_m, h, d), dtype=np.uint8)
+    _check(load_library().mglu_codes_to_bits_host(_ptr(codes), w, n_m, h, d, _ptr(out)), None, "codes_to_bits_host")
+    return out
+
+
+def mglu_pack_codes_host(codes: np.ndarray, w: int, n_m: int, h: int, d: int) -> np.ndarray:
+    """Per-element code stream -> this library's packed layout (d % 32 == 0)."""
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    if codes.size != mglu_code_stream_bytes(d, h, w):
+        raise MgluError(MGLU_ERR_INVALID_ARG, "code stream size mismatch")
+    out = np.empty(mglu_packed_mask_bytes(d, h, n_m), dtype=np.uint8)
+    _check(load_library().mglu_pack_codes_host(_ptr(codes), w, n_m, h, d, _ptr(out)), None, "pack_codes_host")
+    return out
+
+
+def mglu_unpack_codes_host(packed: np.ndarray, n_m: int, h: int, d: int, w: int) -> np.ndarray:
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    out = np.empty(mglu_code_stream_bytes(d, h, w), dtype=np.uint8)
+    _check(load_library().mglu_unpack_codes_host(_ptr(packed), n_m, h, d, w, _ptr(out)), None, "unpack_codes_host")
+    return out
+
+
 def mglu_pack_masks_device(bits: torch.Tensor, stream=None) -> torch.Tensor:
     assert bits.is_cuda and bits.dtype == torch.uint8 and bits.is_contiguous()
     n_m, h, d = bits.shape
@@ -239,6 +275,10 @@ class Mglu:
 
     def set_path(self, path: str) -> None:
         mglu_set_path(self.handle, PATH[path])
+
+    def set_debug(self, flags: int) -> None:
+        """Test hooks (include/mglu.h): 1 = flip mask 1's bit of element (0, 0) during each call."""
+        _check(load_library().mglu_set_debug(self.handle, int(flags)), self.handle, "mglu_set_debug")
 
     def set_variant(self, variant: str) -> None:
         """Partial-mask ablation variant: standard, no_gate_mask, no_value_mask, no_masks."""

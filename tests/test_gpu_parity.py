@@ -105,6 +105,27 @@ def test_partials_vs_independent_value_stream(n_m, dtype):
                                    rtol=0, atol=1e-5 * scale)
 
 
+@pytest.mark.parametrize("n_m", [1, 2, 4, 8])
+@pytest.mark.parametrize("path,B", [("mma", 1), ("mma", 3), ("tcdec", 1), ("tcdec", 9), ("tcgen05", 2), ("tcgen05", 70)])
+def test_fast_path_partials_vs_independent_value_stream(n_m, path, B):
+    """The fast kernels' own value streams (each kernel's epilogue writes s_i = (t + u_i) / 2 and
+    t - s_i instead of y when the partials entry selects it): checked against the oracle's gate and
+    INDEPENDENTLY computed value streams (P2 across implementations, rows a5/a6 on every path)."""
+    from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
+    d, h = 1024, 300                                   # several tiles, ragged rows
+    inp = make_inputs(400 + 13 * n_m + B, B=B, d=d, h=h, n_m=n_m, dtype="bf16")
+    x, Wt = to_device(inp, "bf16")
+    packed = torch.from_numpy(mglu_pack_masks_host(inp["bits"])).cuda()
+    layer = Mglu(d, h, n_m, act="swish", dtype="bf16", path=path)
+    z = layer.forward_partials(x, Wt, packed).cpu().numpy().astype(np.float64)
+    assert layer.last_path() == path
+    _, zr, tr = oracle_forward(inp, "bf16", n_m, "swish", want_partials=True)
+    for b in range(B):
+        scale = np.max(np.abs(tr[b]))
+        # fp32 accumulation of exact bf16 products, order differing from the oracle's: ~1e-6
+        assert np.max(np.abs(z[b] - zr[b])) / scale <= 1e-5, (b, np.max(np.abs(z[b] - zr[b])) / scale)
+
+
 # ---------------------------------------------------------------- bit-exact decoding (P7)
 @pytest.mark.parametrize("n_m", [1, 2, 4, 8])
 def test_one_hot_partials_bit_exact(n_m):

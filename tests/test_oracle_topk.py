@@ -4,7 +4,37 @@ import math
 import numpy as np
 import pytest
 
-from oracle import ACT_SWISH, ACT_SIGMOID, mglu_forward_np, mglu_partials_np, mglu_routed_from_partials, topk_gate
+from fractions import Fraction
+
+from oracle import (ACT_SWISH, ACT_SIGMOID, mglu_forward_np, mglu_partials_np, mglu_routed_from_partials,
+                    router_logits, topk_gate)
+
+
+def test_router_logits_hand_example_and_orientation():
+    """l = x W_r with W_r stored [n_m][d] (reading R16): x = [1, 2, 3],
+    W_r rows [1, 0, -1], [2, 2, 2] -> l = [1 - 3, 2 + 4 + 6] = [-2, 12].  The asymmetric
+    B x d / n_m x d shapes make a transposed operand fail."""
+    l = router_logits(np.array([[1.0, 2.0, 3.0]]), np.array([[1.0, 0.0, -1.0], [2.0, 2.0, 2.0]]))
+    np.testing.assert_array_equal(l, [[-2.0, 12.0]])
+    rng = np.random.default_rng(0)
+    x, Wr = rng.standard_normal((2, 5)), rng.standard_normal((3, 5))
+    assert router_logits(x, Wr).shape == (2, 3)
+    for k in range(5):                                    # one-hot x at k picks column k of W_r
+        e = np.zeros((1, 5)); e[0, k] = 1.0
+        np.testing.assert_array_equal(router_logits(e, Wr)[0], Wr[:, k])
+
+
+def test_router_logits_exact_rational():
+    """Dyadic inputs: every product and partial sum is exact in binary64, so the oracle must equal
+    the exact rational sum."""
+    rng = np.random.default_rng(1)
+    x = rng.integers(-64, 65, (3, 40)) / 16.0
+    Wr = rng.integers(-64, 65, (4, 40)) / 32.0
+    l = router_logits(x, Wr)
+    for b in range(3):
+        for i in range(4):
+            exact = sum(Fraction(float(x[b, k])) * Fraction(float(Wr[i, k])) for k in range(40))
+            assert Fraction(float(l[b, i])) == exact
 
 
 def test_spec_worked_example_k2():
