@@ -135,6 +135,12 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if constexpr (NSPLIT > 1) {
+    // the pair CTA writes partials into this CTA's shared memory (DSMEM): both must have started
+    // (a distributed-shared-memory access needs its target CTA running -- compute-sanitizer racecheck)
+    cluster_arrive();
+    cluster_wait();
+  }
 
   constexpr int HALF = BN / 2;                             // epilogue tokens per masker group
   float yp[HALF / 8][8];                                   // this thread's partial outputs
