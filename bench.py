@@ -544,7 +544,7 @@ def run_mglu(args, ws, rank, local):
         Wt0, codes0 = layers[0]
         layer.bind(x, Wt0, codes0, y, stream=stream)()
         torch.cuda.synchronize()
-        y_full = gather_columns(y, h_total, ws)
+        y_full = gather_columns(y, h_total)
         if rank == 0:
             full = Mglu(d, h_total, n_m, act=act, dtype="bf16", device=local, path=args.path)
             y_ref = torch.empty(B, h_total, device="cuda", dtype=torch.bfloat16)
