@@ -37,19 +37,23 @@
  * Ownership: every data pointer is BORROWED.  The caller allocates x, Wt, packed, out, z (device
  * memory unless the entry point says "host") and keeps them alive until the work queued on
  * `stream` has completed.  A handle owns only its configuration, a TMA-descriptor cache and a
- * small device workspace allocated at create time; mglu_forward never allocates, never frees and
- * never synchronises (it enqueues kernels on `stream` and returns).
+ * device workspace of the batched-decode path (MGLU_PATH_TCDEC), allocated on its first call (or
+ * by mglu_reserve) and grown -- with a stream synchronisation -- only when a larger batch arrives;
+ * otherwise mglu_forward never allocates, never frees and never synchronises (it enqueues kernels
+ * on `stream` and returns).
  *
  * Errors: every call returns mglu_status; nothing throws or aborts across the ABI.  Argument
  * errors are detected before any launch.  Launch failures return MGLU_ERR_CUDA with the CUDA
  * error string available from mglu_last_error(handle).  Faults inside a kernel surface at the
  * caller's next synchronisation, as in CUDA.
  *
- * Threading: a handle is immutable after mglu_create except for mglu_set_path and its internal
- * caches (guarded by a mutex); concurrent mglu_forward calls on different streams are allowed,
- * EXCEPT on MGLU_PATH_TCDEC (which AUTO picks for bf16 and 5 <= B <= 24): its CTAs exchange
- * partial sums through the handle's workspace, so calls on one handle must be stream-ordered --
- * use one handle per concurrently running stream.
+ * Threading: use a handle from ONE stream at a time (one handle per concurrently running stream).
+ * The handle holds per-call state: the batched-decode workspace and tile tickets (MGLU_PATH_TCDEC,
+ * which AUTO picks for bf16 and 5 <= B <= 64, and for n_m = 8 on layers with h >= 8192 from B = 1)
+ * and mglu_forward_host's device staging buffers.  Calls on different handles may run
+ * concurrently on any streams (the kernels never wait on another CTA, so concurrent kernels always
+ * make progress).  mglu_set_path / mglu_set_variant / mglu_set_debug and the descriptor cache are
+ * guarded by a mutex.
  * Streams are `cudaStream_t` passed as void* (NULL = the legacy default stream).
  */
 #ifndef MGLU_H_
@@ -202,6 +206,13 @@ size_t mglu_code_stream_bytes(int64_t d, int64_t h, int w);
 mglu_status mglu_codes_to_bits_host(const uint8_t* codes, int w, int n_m, int64_t h, int64_t d, uint8_t* bits);
 mglu_status mglu_pack_codes_host(const uint8_t* codes, int w, int n_m, int64_t h, int64_t d, uint8_t* packed);
 mglu_status mglu_unpack_codes_host(const uint8_t* packed, int n_m, int64_t h, int64_t d, int w, uint8_t* codes);
+
+/* Pre-allocates the stream-K (MGLU_PATH_TCDEC) workspace for batches up to max_B on `stream`.
+ * Without it the workspace is allocated on the first TCDEC call and grown when a larger batch
+ * arrives (the growing call synchronises `stream`); call this before capturing forwards into a
+ * CUDA graph.  The workspace is (n_m + 1) x {16, 32, 64} x 128 x 8 bytes per SM plus one word per
+ * 128-row tile.  Errors: INVALID_ARG, OOM, CUDA. */
+mglu_status mglu_reserve(mglu_handle hd, int64_t max_B, void* stream);
 
 /* Test hook ("injected mask-corruption flag"): with MGLU_DEBUG_FLIP_MASK_BIT set, every
  * forward / partials call on the handle flips bit 0 of the caller's packed codes -- mask 1 of

@@ -265,6 +265,28 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
     pdl_wait();                                            // out may be read upstream
     const uint32_t lane_base = tmem + lane_off;
     static_assert(HALF % 8 == 0, "BN / 2 must be a multiple of 8");
+    if (p.z) {
+      // partials (debug / parity of a5, a6): this CTA's masks' s_i and t - s_i, no reduction.  A
+      // separate loop: a partials branch inside the y loop below cost the BN = 64 tile 2x (measured)
+      for (int ch = 0; ch < HALF / 8; ++ch) {
+        const int c0 = g * HALF + ch * 8;
+        uint32_t tv[8], uv[8];
+        tmem_ld8(lane_base + c0, tv);
+        for (int i = 0; i < MPC; ++i) {
+          tmem_ld8(lane_base + (1 + i) * BN + c0, uv);
+          tmem_ld_wait();
+          for (int q = 0; q < 8; ++q) {
+            const int tq = n0 + c0 + q;
+            const float t = __uint_as_float(tv[q]), sg = 0.5f * (t + __uint_as_float(uv[q]));
+            if (tq < p.B && m0 + m < p.h) {
+              float* zt = p.z + (size_t)tq * 2 * NM * p.h + m0 + m;
+              zt[(size_t)(moff + i) * p.h] = sg;
+              zt[(size_t)(NM + moff + i) * p.h] = t - sg;
+            }
+          }
+        }
+      }
+    } else
 #pragma unroll
     for (int ch = 0; ch < HALF / 8; ++ch) {
       const int c0 = g * HALF + ch * 8;
@@ -281,14 +303,6 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
 #pragma unroll
         for (int i = 0; i < MPC; ++i) {
           const float sg = 0.5f * (t + __uint_as_float(uv[i][q]));       // s_i = (t + u_i) / 2
-          if (p.z) {                                       // partials: this CTA's masks, no reduction
-            if (tq < p.B && m0 + m < p.h) {
-              float* zt = p.z + (size_t)tq * 2 * NM * p.h + m0 + m;
-              zt[(size_t)(moff + i) * p.h] = sg;
-              zt[(size_t)(NM + moff + i) * p.h] = t - sg;
-            }
-            continue;
-          }
           const float gate = (p.variant & 1) ? t : sg;                    // ablation variants
           const float value = (p.variant & 2) ? t : t - sg;
           const float wgt = p.G ? (tq < p.B ? p.G[(size_t)tq * NM + moff + i] : 0.f) : 1.f;   // routed (App. B)
@@ -296,7 +310,6 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
         }
         yp[ch][q] = acc;
       }
-      if (p.z) continue;
       if constexpr (NSPLIT > 1) {
         if (blockIdx.z == 1) {                             // partial of masks 5..8 -> rank 0's buffer
 #pragma unroll

@@ -62,7 +62,7 @@ struct DecParams {
   int stages;                // ring depth
   int xpar;                  // u32 words per parity array of one token's x in smem (+ pad)
   int l2pf;                  // stages beyond the ring prefetched into L2 once, at the CTA's start
-  float* z;                  // non-null: write Alg. 1's z [B][2 n_m][h] (s_i, t - s_i) instead of y
+  float* z;                  // KSEL = -1 instantiation: Alg. 1's z [B][2 n_m][h] (s_i, t - s_i) instead of y
 };
 
 // One TMA descriptor pair per round type ti (T = 8 >> ti tiles of 8 rows, WPT = 2 << ti warps per
@@ -422,16 +422,14 @@ gemv_mma_kernel(const DecParams p, const __grid_constant__ DecMaps maps) {
           float sv[NSLOT > 0 ? NSLOT : 1];
 #pragma unroll
           for (int ii = 0; ii < NSLOT; ++ii) sv[ii] = 0.5f * (v[nb][0] + v[nb][1 + ii]);   // s_i = (t + u_i) / 2
-          if constexpr (NM > 0 && KSEL == 0) {
-            if (p.z) {                                      // partials (debug / parity of a5, a6)
-              float* zt = p.z + (size_t)tok * 2 * NM * p.h + r0 + row;
+          if constexpr (KSEL < 0) {                        // partials instantiation (debug / parity of a5, a6)
+            float* zt = p.z + (size_t)tok * 2 * NM * p.h + r0 + row;
 #pragma unroll
-              for (int ii = 0; ii < NM; ++ii) {
-                zt[(size_t)ii * p.h] = sv[ii];
-                zt[(size_t)(NM + ii) * p.h] = v[nb][0] - sv[ii];
-              }
-              continue;
+            for (int ii = 0; ii < NM; ++ii) {
+              zt[(size_t)ii * p.h] = sv[ii];
+              zt[(size_t)(NM + ii) * p.h] = v[nb][0] - sv[ii];
             }
+            continue;
           }
           float y;
           if constexpr (NM == 0) {

@@ -52,11 +52,11 @@ struct mglu_ctx {
   };
   std::array<DecMaps, 16> dec_cache;
   uint64_t dec_clock = 0;
-  // stream-K decode (tcgen05) workspace: partial accumulators + one flag per CTA (flags are 0
-  // between calls: the owner CTA re-arms them), grown on demand
+  // stream-K decode (tcgen05) workspace: published partials + one ticket per 128-row tile (0
+  // between calls: a tile's last arriver re-arms it), allocated / grown on first use
   float* sk_ws = nullptr;
   size_t sk_ws_bytes = 0;
-  uint32_t* sk_flags = nullptr;
+  uint32_t* sk_tickets = nullptr;
 
 };
 
@@ -324,6 +324,13 @@ cudaError_t run_mma(mglu_ctx* hd, const void* x, int B, const void* Wt, const vo
         if (u <= 4) return run_mma_nb<NM, ACT, 1, 4>(hd, x, B, Wt, codes, out, cl);
     }
   }
+  if constexpr (NM > 0) {
+    if (cl.z) {                                       // partials: a compile-time instantiation (KSEL = -1)
+      if constexpr (NM >= 4) return B <= 4 ? run_mma_nb<NM, mglu::kIdentity, 1, -1>(hd, x, B, Wt, codes, out, cl) : cudaErrorInvalidValue;
+      else return B <= 4 ? run_mma_nb<NM, mglu::kIdentity, 1, -1>(hd, x, B, Wt, codes, out, cl)
+                         : run_mma_nb<NM, mglu::kIdentity, 2, -1>(hd, x, B, Wt, codes, out, cl);
+    }
+  }
   if constexpr (NM >= 4) return B <= 4 ? run_mma_nb<NM, ACT, 1, 0>(hd, x, B, Wt, codes, out, cl) : cudaErrorInvalidValue;
   else return B <= 4 ? run_mma_nb<NM, ACT, 1, 0>(hd, x, B, Wt, codes, out, cl)
                      : run_mma_nb<NM, ACT, 2, 0>(hd, x, B, Wt, codes, out, cl);
@@ -483,28 +490,32 @@ cudaError_t tc_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const 
 
 // ------------------------------------------------------------------ tcgen05 stream-K decode dispatch
 constexpr int kSkMaxB = 64;
-constexpr int kAutoMmaMaxB = 4, kAutoSkMaxB = 24;
+constexpr int kAutoMmaMaxB = 4, kAutoSkMaxB = 16;
 
 bool sk_can_serve(const mglu_ctx* hd, int64_t B) {
-  // 64-column units; mask-word rows of d/32 * n_m u32 words must be 16-byte multiples (TMA)
+  // 128-column units; mask-word rows of d/32 * n_m u32 words must be 16-byte multiples (TMA)
   return hd->dtype == MGLU_BF16 && fast_nm(hd->n_m) && hd->d % 64 == 0 && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 &&
          B <= kSkMaxB && (hd->n_m < 8 || B <= 32);
 }
 
-// workspace of the stream-K decode path, allocated once at mglu_create for the largest batch the
-// path serves: G x (n_m + 1) x B x 128 fp32 partials and G flags (zeroed; owners re-arm them)
-cudaError_t sk_alloc(mglu_ctx* hd) {
-  const size_t G = (size_t)hd->num_sms;
-  const size_t maxb = !fast_nm(hd->n_m) ? 0 : hd->n_m == 8 ? 32 : kSkMaxB;   // (SIMT-only counts: no stream-K)
-  cudaError_t e = cudaMalloc(&hd->sk_flags, G * sizeof(uint32_t));
-  if (e != cudaSuccess) return e;
-  e = cudaMemset(hd->sk_flags, 0, G * sizeof(uint32_t));
-  if (e != cudaSuccess) return e;
-  hd->sk_ws_bytes = G * (size_t)(hd->n_m + 1) * maxb * 128 * sizeof(float);
-  if (!hd->sk_ws_bytes) return cudaSuccess;
-  e = cudaMalloc(&hd->sk_ws, hd->sk_ws_bytes);
-  if (e != cudaSuccess) hd->sk_ws_bytes = 0;
-  return e;
+// stream-K workspace, grown on demand (the first call of a larger batch): 2 published partials per
+// CTA (its first and last segments) of (n_m + 1) x B x 128 fp32, and one ticket per 128-row tile
+// (zeroed once; the last arriver of a tile re-arms it)
+cudaError_t sk_workspace(mglu_ctx* hd, size_t ws_bytes, cudaStream_t st) {
+  const size_t tiles = (size_t)((hd->h + 127) / 128);
+  if (!hd->sk_tickets) {
+    cudaError_t e = cudaMalloc(&hd->sk_tickets, tiles * sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(hd->sk_tickets, 0, tiles * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+  }
+  if (hd->sk_ws_bytes < ws_bytes) {
+    if (hd->sk_ws) { cudaStreamSynchronize(st); cudaFree(hd->sk_ws); hd->sk_ws = nullptr; hd->sk_ws_bytes = 0; }
+    cudaError_t e = cudaMalloc(&hd->sk_ws, ws_bytes);
+    if (e != cudaSuccess) return e;
+    hd->sk_ws_bytes = ws_bytes;
+  }
+  return cudaSuccess;
 }
 
 template <int NM, int BN, int MG>
@@ -516,7 +527,7 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   constexpr int KB = C::KS / 64;
   if (!encode_3d_blocks(&mW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, 128, KB, sw) ||
       !encode_3d_blocks(&mX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, hd->d, B, 64, BN, KB, sw) ||
-      !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, C::CW, 128, code_swizzle(C::CW * 4)))
+      !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, C::CWORDS, 128, code_swizzle(C::CWORDS * 4)))
     return cudaErrorInvalidValue;
   mglu::SkParams p;
   p.out = (__nv_bfloat16*)out;
@@ -532,17 +543,18 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   const int64_t G = std::min<int64_t>(hd->num_sms, units);
   p.units_base = (int)(units / G);
   p.units_rem = (int)(units % G);
-  if (!hd->sk_flags || hd->sk_ws_bytes < (size_t)G * C::NOP * B * 128 * sizeof(float)) return cudaErrorInvalidValue;
+  cudaError_t e = sk_workspace(hd, (size_t)hd->num_sms * 2 * C::NOP * BN * 128 * sizeof(float), cl.st);
+  if (e != cudaSuccess) return e;
   p.ws = hd->sk_ws;
-  p.flags = hd->sk_flags;
-  const size_t fixed = 1024 + 512;                          // alignment slack + barriers + TMEM slot
+  p.tickets = hd->sk_tickets;
   const size_t cap = (size_t)hd->max_smem_optin;
-  if (cap < fixed + 2 * (size_t)C::SB) return cudaErrorInvalidConfiguration;
-  const int S = (int)std::min<size_t>(16, (cap - fixed) / C::SB);
-  p.stages = S;
-  const size_t smem = (size_t)S * C::SB + fixed;
+  p.xstages = 4;
+  const size_t fixed = 1024 + 256 + (size_t)p.xstages * C::XB;   // alignment slack + barriers + x ring
+  if (cap < fixed + 2 * (size_t)C::WSB) return cudaErrorInvalidConfiguration;
+  p.wstages = (int)std::min<size_t>(8, (cap - fixed) / C::WSB);
+  const size_t smem = (size_t)p.wstages * C::WSB + fixed;
   auto kern = mglu::gemv_tc_kernel<NM, BN, MG>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(kern, dim3((unsigned)G), dim3(C::THREADS), smem, cl.st, p, mW, mX, mC);
 }
@@ -659,18 +671,22 @@ mglu_status mglu_create(mglu_handle* out, int64_t d, int64_t h, int n_m, int act
   hd->d = d; hd->h = h; hd->n_m = n_m; hd->act = act; hd->dtype = dtype; hd->device = device;
   hd->num_sms = prop.multiProcessorCount;
   hd->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
-  if (dtype == MGLU_BF16) {
-    int prev = 0;
-    cudaGetDevice(&prev);
-    cudaSetDevice(device);
-    const cudaError_t e = sk_alloc(hd);
-    cudaSetDevice(prev);
-    if (e != cudaSuccess) {
-      mglu_destroy(hd);
-      return e == cudaErrorMemoryAllocation ? MGLU_ERR_OOM : MGLU_ERR_CUDA;
-    }
-  }
   *out = hd;
+  return MGLU_OK;
+}
+
+mglu_status mglu_reserve(mglu_handle hd, int64_t max_B, void* stream) {
+  if (!hd || max_B < 0) return MGLU_ERR_INVALID_ARG;
+  if (hd->dtype != MGLU_BF16 || !fast_nm(hd->n_m) || max_B == 0) return MGLU_OK;   // no stream-K path
+  const int64_t b = std::min<int64_t>(max_B, hd->n_m == 8 ? 32 : kSkMaxB);
+  const int64_t bn = b <= 16 ? 16 : b <= 32 ? 32 : 64;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != hd->device) cudaSetDevice(hd->device);
+  const cudaError_t e = sk_workspace(hd, (size_t)hd->num_sms * 2 * (hd->n_m + 1) * bn * 128 * sizeof(float),
+                                     (cudaStream_t)stream);
+  if (prev != hd->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? MGLU_ERR_OOM : cuda_fail(hd, e, "mglu_reserve");
   return MGLU_OK;
 }
 
@@ -682,7 +698,7 @@ mglu_status mglu_destroy(mglu_handle hd) {
   if (hd->x_stage) cudaFree(hd->x_stage);
   if (hd->y_stage) cudaFree(hd->y_stage);
   if (hd->sk_ws) cudaFree(hd->sk_ws);
-  if (hd->sk_flags) cudaFree(hd->sk_flags);
+  if (hd->sk_tickets) cudaFree(hd->sk_tickets);
   cudaSetDevice(prev);
   delete hd;
   return MGLU_OK;
@@ -731,12 +747,12 @@ static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, con
     path = MGLU_PATH_MMA;
   }
   if (path == MGLU_PATH_AUTO) {
-    // measured crossovers at the Llama-3-8B FFN shape (profiles/r01_paths_by_batch.txt): the
+    // measured crossovers at the Llama-3-8B FFN shape (profiles/r02/paths_by_batch.txt): the
     // register-masked HMMA kernel for B <= 4 (one 8-column MMA tile), the stream-K tcgen05 GEMV for
-    // 5 <= B <= 24, the tcgen05 tile GEMM above; SIMT for fp32 and shapes the others refuse
+    // 5 <= B <= 16, the tcgen05 tile GEMM above; SIMT for fp32 and shapes the others refuse
     // (n_m = 8 on large layers: the HMMA kernel's 9 MMAs per step make it compute-bound, and the
-    //  tcgen05 GEMV wins from B = 1: 151 vs 161 us at d=8192 h=28672, 41.5 vs 43.7 at the config-3
-    //  shape; on small shards (h < 8192) the HMMA kernel stays ahead)
+    //  tcgen05 GEMV wins from B = 1: 132 vs 139 us at d=8192 h=28672; on small shards (h < 8192)
+    //  the HMMA kernel stays ahead)
     const bool nm8_big = hd->n_m == 8 && hd->h >= 8192 && sk_can_serve(hd, B);
     if (B <= kAutoMmaMaxB && mma_can_serve(hd, B) && !nm8_big)
       path = MGLU_PATH_MMA;

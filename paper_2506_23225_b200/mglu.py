@@ -62,6 +62,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "mglu_set_path": ([vp, c_int], c_int),
         "mglu_set_variant": ([vp, c_int], c_int),
         "mglu_set_debug": ([vp, c_int], c_int),
+        "mglu_reserve": ([vp, i64, vp], c_int),
         "mglu_forward": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_forward_partials": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_forward_host": ([vp, vp, i64, vp, vp, vp, vp], c_int),
@@ -275,6 +276,11 @@ class Mglu:
 
     def set_path(self, path: str) -> None:
         mglu_set_path(self.handle, PATH[path])
+
+    def reserve(self, max_B: int, stream=None) -> None:
+        """Pre-allocate the batched-decode workspace for batches up to max_B (before graph capture)."""
+        _check(load_library().mglu_reserve(self.handle, int(max_B), _stream_ptr(stream, torch.device("cuda", self.device))),
+               self.handle, "mglu_reserve")
 
     def set_debug(self, flags: int) -> None:
         """Test hooks (include/mglu.h): 1 = flip mask 1's bit of element (0, 0) during each call."""

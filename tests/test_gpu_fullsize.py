@@ -110,7 +110,7 @@ def test_full_size_tensor_core_sampled(name, d, h, n_m, B):
     layer = Mglu(d, h, n_m, act="swish", dtype="bf16")
     y = layer.forward(x, Wt, packed)
     torch.cuda.synchronize()
-    assert layer.last_path() == ("tcdec" if B <= 24 else "tcgen05")
+    assert layer.last_path() == ("tcdec" if B <= 16 else "tcgen05")
     rng = np.random.default_rng(B + n_m)
     toks = np.unique(np.concatenate([[0, B - 1], rng.choice(B, min(B, 46), replace=False)]))
     cols = np.unique(np.concatenate([[0, 127, 128, h - 1], rng.choice(h, 92, replace=False)]))

@@ -191,6 +191,6 @@ def test_routed_forward_large_batch_auto(B):
     layer = Mglu(d, h, n_m, act="swish", dtype="bf16")
     y = layer.forward_routed(x, Wt, packed, torch.from_numpy(G).cuda(), K)
     torch.cuda.synchronize()
-    assert layer.last_path() == ("tcdec" if B <= 24 else "tcgen05")
+    assert layer.last_path() == ("tcdec" if B <= 16 else "tcgen05")
     ref = _oracle_routed(inp, n_m, 1, G.astype(np.float64))
     assert normwise_err(y.float().cpu().numpy().astype(np.float64), ref) <= TIGHT["bf16"]

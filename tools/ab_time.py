@@ -59,13 +59,23 @@ def run(name, K):
     return e0.elapsed_time(e1) * 1e3 / K
 
 
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    _nv = pynvml.nvmlDeviceGetHandleByIndex(0)
+    clk = lambda: pynvml.nvmlDeviceGetClockInfo(_nv, pynvml.NVML_CLOCK_SM)   # noqa: E731
+except Exception:  # noqa: BLE001
+    clk = lambda: -1   # noqa: E731
 for name in libs:
     run(name, 20)
 res = {n: [] for n in libs}
+clocks = []
 for rep in range(a.reps):
     for name in libs:
         res[name].append(run(name, a.steps))
+        clocks.append(clk())
 ab = h * d * 2 + h * d * n_m // 8 + B * d * 2 + B * h * 2
 for name, v in res.items():
     m = statistics.median(v)
-    print(f"{name:24s} median {m:7.2f} us  min {min(v):7.2f}  max {max(v):7.2f}  {ab / m / 1e3:7.0f} GB/s")
+    print(f"{name:24s} median {m:7.2f} us  min {min(v):7.2f}  max {max(v):7.2f}  {ab / m / 1e3:7.0f} GB/s"
+          f"  {2 * B * d * h * (n_m + 1) / m / 1e6:7.1f} TFLOP/s  sm_mhz after reps {clocks}")
