@@ -207,6 +207,22 @@ mglu_status mglu_codes_to_bits_host(const uint8_t* codes, int w, int n_m, int64_
 mglu_status mglu_pack_codes_host(const uint8_t* codes, int w, int n_m, int64_t h, int64_t d, uint8_t* packed);
 mglu_status mglu_unpack_codes_host(const uint8_t* packed, int n_m, int64_t h, int64_t d, int w, uint8_t* codes);
 
+/* Training path (Alg. 2: hard masks in the forward, the
+ * straight-through estimator hands dL/dM_i to the soft logits unchanged; reading R21).  Given the
+ * layer's inputs and the upstream gradient dy = dL/dy:
+ *   x [B][d], Wt [h][d]  handle dtype (bf16 / fp32), packed masks as for mglu_forward;
+ *   dy [B][h] fp32;
+ *   dx [B][d], dW [h][d], dlogits [n_m][h][d] fp32 outputs, each optional (NULL skips it).
+ * Recomputes the forward streams s_i, v_i with the forward kernels (partials mode, the path the
+ * handle would take), then a_i = dy g'(s_i) v_i, c_i = dy g(s_i) and
+ *   dx = sum_i a_i (M_i (.) W) + c_i (Mbar_i (.) W),   dW = sum_i M_i (.) a_i^T x + Mbar_i (.) c_i^T x,
+ *   dlogits_i = W (.) (a_i - c_i)^T x.
+ * fp32 accumulation, deterministic.  n_m in {1, 2, 4, 8}.  Uses a handle workspace of
+ * (3 n_m + 1) B h floats (grown on demand, the growing call synchronises `stream`).
+ * Errors: INVALID_ARG, UNSUPPORTED, OOM, CUDA; plus those of the forward. */
+mglu_status mglu_backward(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* packed,
+                          const float* dy, float* dx, float* dW, float* dlogits, void* stream);
+
 /* Pre-allocates the stream-K (MGLU_PATH_TCDEC) workspace for batches up to max_B on `stream`.
  * Without it the workspace is allocated on the first TCDEC call and grown when a larger batch
  * arrives (the growing call synchronises `stream`); call this before capturing forwards into a

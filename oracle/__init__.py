@@ -11,6 +11,7 @@ Contents
   * ``mglu_oracle.c`` (+ ``c_oracle``) -- plain C, binary64 loops, OpenMP over output columns.
   * ``accounting``  -- closed forms of Table 1 / Sec. 4.1 (memory load, parameters, FLOPs).
   * ``codes``       -- per-element mask code streams.
+  * ``backward``    -- the training path: Eq. 3's gradients under Alg. 2's STE.
 
 Every function cites the PAPER.md passage it follows (``P:<line>``).  DESIGN.md lists the
 readings (R1..R15) taken where the paper is silent or garbled.
@@ -28,3 +29,4 @@ from .topk import router_logits, topk_gate, mglu_routed_from_partials  # noqa: F
 from .ffn import ffn_forward_np, dense_np  # noqa: F401,E402
 from .variants import VARIANTS, mglu_variant_from_streams  # noqa: F401,E402
 from .codes import codes_to_bits_np, bits_to_codes_np  # noqa: F401,E402
+from .backward import act_grad_np, mglu_backward_np, relaxed_forward_np  # noqa: F401,E402

@@ -62,6 +62,7 @@ struct DecParams {
   int stages;                // ring depth
   int xpar;                  // u32 words per parity array of one token's x in smem (+ pad)
   int l2pf;                  // stages beyond the ring prefetched into L2 once, at the CTA's start
+  int light_drop;            // stages fewer in flight for the CTAs owning tiles_base tiles
   float* z;                  // KSEL = -1 instantiation: Alg. 1's z [B][2 n_m][h] (s_i, t - s_i) instead of y
 };
 
@@ -118,7 +119,10 @@ gemv_mma_kernel(const DecParams p, const __grid_constant__ DecMaps maps) {
   // (17 warps per CTA leave 96 registers per thread: one SM sub-partition holds 5 of them.)
   constexpr int kGrp = (NB == 2 && (KSEL > 0 ? KSEL : NM) >= 4) ? 1 : ((KSEL > 0 ? KSEL : NM) * NB > 4) ? 2 : 4;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int S = p.stages;
+  // ring depth: the CTAs owning one tile more than the others keep one stage more in flight, so
+  // their share of the HBM bandwidth grows with their work and they do not finish last (the next
+  // call's consumers wait for this grid's last CTA)
+  const int S = (p.tiles_rem && (int)blockIdx.x >= p.tiles_rem) ? p.stages - p.light_drop : p.stages;
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB);
   uint64_t* empty = full + S;

@@ -24,6 +24,7 @@
 #include "gemv_tc.cuh"
 #include "pack.cuh"
 #include "router.cuh"
+#include "backward.cuh"
 
 
 struct mglu_ctx {
@@ -57,6 +58,9 @@ struct mglu_ctx {
   float* sk_ws = nullptr;
   size_t sk_ws_bytes = 0;
   uint32_t* sk_tickets = nullptr;
+  // training path (mglu_backward): forward streams z [B][2 n_m][h] + coefficients E [B][n_m+1][h]
+  float* bw_ws = nullptr;
+  size_t bw_ws_bytes = 0;
 
 };
 
@@ -247,6 +251,18 @@ int dec_smem_kb() {
   return v;
 }
 
+// deeper ring for the CTAs with one tile more (MGLU_DEC_HEAVY=0 disables)
+#ifndef MGLU_DEC_HEAVY_DEFAULT
+#define MGLU_DEC_HEAVY_DEFAULT 1
+#endif
+int dec_heavy() {
+  static const int v = [] {
+    const char* e = getenv("MGLU_DEC_HEAVY");
+    return e ? atoi(e) : MGLU_DEC_HEAVY_DEFAULT;
+  }();
+  return v;
+}
+
 // one-shot L2 prefetch depth of the decode kernel (stages past the ring; MGLU_DEC_L2PF overrides)
 int dec_l2pf() {
   static const int v = [] {
@@ -275,6 +291,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   p.tiles_base = (int)(tiles / ncta);
   p.tiles_rem = (int)(tiles % ncta);
   p.l2pf = dec_l2pf();
+  p.light_drop = 0;
   mglu::DecMaps maps;
   if (!dec_maps(hd, Wt, codes, &maps)) return cudaErrorInvalidValue;
   // x in smem, split by pair parity and zero-padded to the last column any stage can touch (the
@@ -301,7 +318,13 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   S = std::min(8, S);
   if (S < 2) return cudaErrorInvalidConfiguration;
   p.stages = S;
-  const size_t smem = (size_t)S * SB + 2 * S * sizeof(uint64_t) + partbytes + xbytes;
+  // heavier CTAs (tiles_base + 1 tiles) one stage deeper than the light ones when a stage fits
+  // beside the light CTAs' ring (MGLU_DEC_HEAVY=0 disables, for experiments)
+  if (p.tiles_rem && dec_heavy() && S >= 3 && S < 8 && (size_t)(S + 1) * (SB + 16) + fixed <= (size_t)hd->max_smem_optin) {
+    p.stages = S + 1;
+    p.light_drop = 1;
+  }
+  const size_t smem = (size_t)p.stages * SB + 2 * p.stages * sizeof(uint64_t) + partbytes + xbytes;
   auto kern = mglu::gemv_mma_kernel<NM, ACT, NB, KSEL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -699,6 +722,7 @@ mglu_status mglu_destroy(mglu_handle hd) {
   if (hd->y_stage) cudaFree(hd->y_stage);
   if (hd->sk_ws) cudaFree(hd->sk_ws);
   if (hd->sk_tickets) cudaFree(hd->sk_tickets);
+  if (hd->bw_ws) cudaFree(hd->bw_ws);
   cudaSetDevice(prev);
   delete hd;
   return MGLU_OK;
@@ -732,6 +756,29 @@ int mglu_last_path(mglu_handle hd) { return hd ? hd->last_path : -1; }
 
 // the forward on an explicit path (AUTO resolved here); shared by mglu_forward and
 // mglu_forward_routed
+// AUTO: the path mglu_forward takes for this handle and batch
+static int auto_path(const mglu_ctx* hd, int64_t B) {
+  int path;
+  // measured crossovers at the Llama-3-8B FFN shape (profiles/r02/paths_by_batch.txt): the
+  // register-masked HMMA kernel for B <= 4 (one 8-column MMA tile), the stream-K tcgen05 GEMV for
+  // 5 <= B <= 16, the tcgen05 tile GEMM above; SIMT for fp32 and shapes the others refuse
+  // (n_m = 8 on large layers: the HMMA kernel's 9 MMAs per step make it compute-bound, and the
+  //  tcgen05 GEMV wins from B = 1: 132 vs 139 us at d=8192 h=28672; on small shards (h < 8192)
+  //  the HMMA kernel stays ahead)
+  const bool nm8_big = hd->n_m == 8 && hd->h >= 8192 && sk_can_serve(hd, B);
+  if (B <= kAutoMmaMaxB && mma_can_serve(hd, B) && !nm8_big)
+    path = MGLU_PATH_MMA;
+  else if (B <= kAutoSkMaxB && sk_can_serve(hd, B))
+    path = MGLU_PATH_TCDEC;
+  else if (mma_can_serve(hd, B))
+    path = MGLU_PATH_MMA;
+  else if (tc_can_serve(hd, B))
+    path = MGLU_PATH_TCGEN05;
+  else
+    path = MGLU_PATH_SIMT;
+  return path;
+}
+
 // test hook: flip one bit of the caller's packed codes (mglu_set_debug)
 __global__ void flip_bit_kernel(uint8_t* p, uint8_t m) { p[0] ^= m; }
 
@@ -746,25 +793,7 @@ static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, con
       return set_err(hd, MGLU_ERR_UNSUPPORTED, "dense (n_m = 0) handles: MMA path, bf16, 1 <= B <= 8, d % 128 == 0");
     path = MGLU_PATH_MMA;
   }
-  if (path == MGLU_PATH_AUTO) {
-    // measured crossovers at the Llama-3-8B FFN shape (profiles/r02/paths_by_batch.txt): the
-    // register-masked HMMA kernel for B <= 4 (one 8-column MMA tile), the stream-K tcgen05 GEMV for
-    // 5 <= B <= 16, the tcgen05 tile GEMM above; SIMT for fp32 and shapes the others refuse
-    // (n_m = 8 on large layers: the HMMA kernel's 9 MMAs per step make it compute-bound, and the
-    //  tcgen05 GEMV wins from B = 1: 132 vs 139 us at d=8192 h=28672; on small shards (h < 8192)
-    //  the HMMA kernel stays ahead)
-    const bool nm8_big = hd->n_m == 8 && hd->h >= 8192 && sk_can_serve(hd, B);
-    if (B <= kAutoMmaMaxB && mma_can_serve(hd, B) && !nm8_big)
-      path = MGLU_PATH_MMA;
-    else if (B <= kAutoSkMaxB && sk_can_serve(hd, B))
-      path = MGLU_PATH_TCDEC;
-    else if (mma_can_serve(hd, B))
-      path = MGLU_PATH_MMA;
-    else if (tc_can_serve(hd, B))
-      path = MGLU_PATH_TCGEN05;
-    else
-      path = MGLU_PATH_SIMT;
-  }
+  if (path == MGLU_PATH_AUTO) path = auto_path(hd, B);
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != hd->device) cudaSetDevice(hd->device);
@@ -895,6 +924,85 @@ mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, cons
   cl.st = (cudaStream_t)stream;
   cl.z = z;
   return forward_on_path(hd, x, B, Wt, packed, nullptr, path, cl);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ training path (row f4)
+template <typename T, int NM>
+static cudaError_t backward_kernels(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* packed,
+                                    const float* dy, float* dx, float* dW, float* dlogits, const float* z, float* E,
+                                    cudaStream_t st) {
+  const int d = (int)hd->d, h = (int)hd->h;
+  const int64_t n = (int64_t)B * h;
+  mglu::coef_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)hd->num_sms * 16), 256, 0, st>>>(
+      z, dy, B, h, NM, hd->act, E);
+  if (dW || dlogits)
+    mglu::dw_kernel<T, NM><<<dim3((unsigned)((d + mglu::kBwK - 1) / mglu::kBwK), (unsigned)((h + mglu::kBwJ - 1) / mglu::kBwJ)),
+                             256, 0, st>>>((const T*)x, (const T*)Wt, (const uint32_t*)packed, E, B, d, h, dW, dlogits);
+  if (dx)
+    mglu::dx_kernel<T, NM><<<dim3((unsigned)((d + mglu::kBwK - 1) / mglu::kBwK), (unsigned)((B + mglu::kBwB - 1) / mglu::kBwB)),
+                             256, 0, st>>>((const T*)Wt, (const uint32_t*)packed, E, B, d, h, dx);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t backward_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* packed, const float* dy,
+                               float* dx, float* dW, float* dlogits, const float* z, float* E, cudaStream_t st) {
+  switch (hd->n_m) {
+    case 1: return backward_kernels<T, 1>(hd, x, B, Wt, packed, dy, dx, dW, dlogits, z, E, st);
+    case 2: return backward_kernels<T, 2>(hd, x, B, Wt, packed, dy, dx, dW, dlogits, z, E, st);
+    case 4: return backward_kernels<T, 4>(hd, x, B, Wt, packed, dy, dx, dW, dlogits, z, E, st);
+    case 8: return backward_kernels<T, 8>(hd, x, B, Wt, packed, dy, dx, dW, dlogits, z, E, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+extern "C" {
+
+mglu_status mglu_backward(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* packed,
+                                     const float* dy, float* dx, float* dW, float* dlogits, void* stream) {
+  if (!hd) return MGLU_ERR_INVALID_ARG;
+  if (!x || !Wt || !packed || !dy || B < 0) return set_err(hd, MGLU_ERR_INVALID_ARG, "null pointer or B < 0");
+  if (!fast_nm(hd->n_m)) return set_err(hd, MGLU_ERR_UNSUPPORTED, "backward: n_m in {1, 2, 4, 8}");
+  if (B > (int64_t)1 << 30) return set_err(hd, MGLU_ERR_INVALID_ARG, "B too large");
+  hd->last_launches = 0;
+  if (B == 0) return MGLU_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != hd->device) cudaSetDevice(hd->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t zf = (size_t)B * 2 * hd->n_m * hd->h, ef = (size_t)B * (hd->n_m + 1) * hd->h;
+  const size_t need = (zf + ef) * sizeof(float);
+  if (hd->bw_ws_bytes < need) {
+    if (hd->bw_ws) { cudaStreamSynchronize(st); cudaFree(hd->bw_ws); hd->bw_ws = nullptr; hd->bw_ws_bytes = 0; }
+    if (cudaMalloc(&hd->bw_ws, need) != cudaSuccess) {
+      if (prev != hd->device) cudaSetDevice(prev);
+      return set_err(hd, MGLU_ERR_OOM, "backward workspace");
+    }
+    hd->bw_ws_bytes = need;
+  }
+  float* z = hd->bw_ws;
+  float* E = hd->bw_ws + zf;
+  // the forward streams s_i, v_i from the forward kernels' partials mode (the path AUTO would take)
+  int path;
+  {
+    std::lock_guard<std::mutex> g(hd->mu);
+    path = hd->path;
+  }
+  if (path == MGLU_PATH_AUTO) path = auto_path(hd, B);
+  Call cl;
+  cl.st = st;
+  cl.z = z;
+  mglu_status s = forward_on_path(hd, x, B, Wt, packed, nullptr, path, cl);
+  if (s != MGLU_OK) { if (prev != hd->device) cudaSetDevice(prev); return s; }
+  const cudaError_t e = hd->dtype == MGLU_BF16
+                            ? backward_nm<__nv_bfloat16>(hd, x, (int)B, Wt, packed, dy, dx, dW, dlogits, z, E, st)
+                            : backward_nm<float>(hd, x, (int)B, Wt, packed, dy, dx, dW, dlogits, z, E, st);
+  if (prev != hd->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(hd, e, "mglu_backward launch");
+  hd->last_launches = 2 + (dW || dlogits ? 1 : 0) + (dx ? 1 : 0);
+  return MGLU_OK;
 }
 
 mglu_status mglu_forward_host(mglu_handle hd, const void* x_host, int64_t B, const void* Wt,

@@ -63,6 +63,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "mglu_set_variant": ([vp, c_int], c_int),
         "mglu_set_debug": ([vp, c_int], c_int),
         "mglu_reserve": ([vp, i64, vp], c_int),
+        "mglu_backward": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp], c_int),
         "mglu_forward": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_forward_partials": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_forward_host": ([vp, vp, i64, vp, vp, vp, vp], c_int),
@@ -276,6 +277,22 @@ class Mglu:
 
     def set_path(self, path: str) -> None:
         mglu_set_path(self.handle, PATH[path])
+
+    def backward(self, x: torch.Tensor, Wt: torch.Tensor, packed: torch.Tensor, dy: torch.Tensor,
+                 want=("dx", "dW", "dlogits"), stream=None):
+        """Gradients of Eq. 3 under Alg. 2's STE (row f4): returns (dx [B][d], dW [h][d],
+        dlogits [n_m][h][d]) fp32, None for the ones not in `want`."""
+        self._check_inputs(x, Wt, packed)
+        B = x.shape[0]
+        if dy.dtype != torch.float32 or tuple(dy.shape) != (B, self.h) or not dy.is_contiguous() or dy.device != x.device:
+            raise MgluError(MGLU_ERR_INVALID_ARG, "dy must be a contiguous fp32 [B][h] tensor on x's device")
+        f32 = dict(dtype=torch.float32, device=x.device)
+        dx = torch.empty((B, self.d), **f32) if "dx" in want else None
+        dW = torch.empty((self.h, self.d), **f32) if "dW" in want else None
+        dl = torch.empty((self.n_m, self.h, self.d), **f32) if "dlogits" in want else None
+        _check(load_library().mglu_backward(self.handle, _ptr(x), B, _ptr(Wt), _ptr(packed), _ptr(dy), _ptr(dx), _ptr(dW),
+                                            _ptr(dl), _stream_ptr(stream, x.device)), self.handle, "mglu_backward")
+        return dx, dW, dl
 
     def reserve(self, max_B: int, stream=None) -> None:
         """Pre-allocate the batched-decode workspace for batches up to max_B (before graph capture)."""
