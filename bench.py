@@ -611,7 +611,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["mglu", "reference"], default="mglu")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
-    ap.add_argument("--path", choices=["auto", "mma", "simt", "tcgen05", "tcdec"], default="auto")
+    ap.add_argument("--path", choices=["auto", "mma", "simt", "tcgen05", "tcdec", "tcrow"], default="auto")
     ap.add_argument("--layers", type=int, default=4, help="distinct layer copies rotated (L2 hygiene)")
     ap.add_argument("--clock-window", type=float, default=0.0,
                     help="seconds of extra steps before the timed region (pre-heats the GPU; default none)")

@@ -97,7 +97,10 @@ typedef enum {
   MGLU_PATH_SIMT = 1,     /* CUDA-core fused masked GEMV (Alg. 1 without split-K), any dtype/B   */
   MGLU_PATH_MMA = 2,      /* register-masked mma.sync GEMV, bf16, streams W+codes once per 8 tok */
   MGLU_PATH_TCGEN05 = 3,  /* tcgen05/TMEM masked GEMM, bf16, prefill / large B                  */
-  MGLU_PATH_TCDEC = 4     /* tcgen05 stream-K masked GEMV, bf16, decode 1 <= B <= 64             */
+  MGLU_PATH_TCDEC = 4,    /* tcgen05 stream-K masked GEMV, bf16, decode 1 <= B <= 64             */
+  MGLU_PATH_TCROW = 5     /* tcgen05 row-split masked GEMV (same kernel, each CTA owns whole     *
+                           * row tiles over all of d: no cross-CTA reduction), bf16, 1 <= B <= 64,
+                           * n_m <= 8 (B <= 32 at n_m = 8)                                          */
 } mglu_path;
 
 /* Create a handle for one (d, h, n_m, act, dtype) layer on CUDA device `device`.

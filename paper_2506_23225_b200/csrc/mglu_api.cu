@@ -72,6 +72,7 @@ struct Call {
   const float* G = nullptr;   // routed gate weights [B][n_m] (mglu_forward_routed), nullptr: Eq. 3
   int K = 0;                  // K of the routed call (0: unknown -> every mask evaluated)
   float* z = nullptr;         // mglu_forward_partials: Alg. 1's z [B][2 n_m][h] instead of y
+  bool row_split = false;     // tcgen05 GEMV: row split (MGLU_PATH_TCROW) instead of stream-K
 };
 
 const char* kStatusStr[] = {"MGLU_OK", "MGLU_ERR_INVALID_ARG", "MGLU_ERR_UNSUPPORTED",
@@ -513,7 +514,7 @@ cudaError_t tc_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const 
 
 // ------------------------------------------------------------------ tcgen05 stream-K decode dispatch
 constexpr int kSkMaxB = 64;
-constexpr int kAutoMmaMaxB = 4, kAutoSkMaxB = 16;
+constexpr int kAutoMmaMaxB = 4, kAutoSkMaxB = 16, kAutoRowMaxB = 48;
 
 bool sk_can_serve(const mglu_ctx* hd, int64_t B) {
   // 128-column units; mask-word rows of d/32 * n_m u32 words must be 16-byte multiples (TMA)
@@ -541,17 +542,41 @@ cudaError_t sk_workspace(mglu_ctx* hd, size_t ws_bytes, cudaStream_t st) {
   return cudaSuccess;
 }
 
+// row split (each tile owned by one CTA over the whole d: no cross-CTA reduction, no workspace,
+// k-order independent of h) when every SM gets at least kSkRowMin rows; stream-K below that (small
+// shards, where 128-row tiles would leave the maskers mostly idle rows)
+constexpr int64_t kSkRowMin = 64;
+int sk_rows_env() {
+  static const int v = [] {
+    const char* e = getenv("MGLU_SK_ROWS");   // experiments / tests: 0 forces stream-K, 1 the row split
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+int sk_max_wstages() {
+  static const int v = [] {
+    const char* e = getenv("MGLU_SK_WSTAGES");   // experiments: W ring depth cap
+    return e ? atoi(e) : 5;   // 5: measured (row split at B = 16: 35.0 us vs 35.7 with 6)
+  }();
+  return v;
+}
+// AUTO's choice between the two forms of the tcgen05 GEMV (profiles/r02/tcrow_sweep.txt, config 3):
+// the row split wins once the stream-K fix-up grows with B (from B = 5, tied there) on layers wide enough to give
+// every SM kSkRowMin rows; at n_m = 8 the maskers' cost per 128-row unit dominates and the row
+// split's partly idle lanes lose (config 5, B = 1: 159 vs 129 us)
+bool auto_row_split(const mglu_ctx* hd, int64_t B) {
+  const int env = sk_rows_env();
+  if (env >= 0) return env == 1;
+  return hd->n_m <= 4 && B >= 5 && hd->h >= (int64_t)hd->num_sms * kSkRowMin;
+}
+
 template <int NM, int BN, int MG>
 cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
                       const Call& cl) {
   using C = mglu::SkCfg<NM, BN, MG>;
-  CUtensorMap mW, mX, mC;
+  CUtensorMap mW, mX, mC, mWb, mCb;
   const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
   constexpr int KB = C::KS / 64;
-  if (!encode_3d_blocks(&mW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, 128, KB, sw) ||
-      !encode_3d_blocks(&mX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, hd->d, B, 64, BN, KB, sw) ||
-      !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, C::CWORDS, 128, code_swizzle(C::CWORDS * 4)))
-    return cudaErrorInvalidValue;
   mglu::SkParams p;
   p.out = (__nv_bfloat16*)out;
   p.G = cl.G;
@@ -562,24 +587,73 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   p.h = (int)hd->h;
   p.act = hd->act;
   p.upt = (int)((hd->d + C::KS - 1) / C::KS);   // a final partial unit reads zero-filled boxes
-  const int64_t units = (hd->h + 127) / 128 * p.upt;
-  const int64_t G = std::min<int64_t>(hd->num_sms, units);
-  p.units_base = (int)(units / G);
-  p.units_rem = (int)(units % G);
-  cudaError_t e = sk_workspace(hd, (size_t)hd->num_sms * 2 * C::NOP * BN * 128 * sizeof(float), cl.st);
-  if (e != cudaSuccess) return e;
-  p.ws = hd->sk_ws;
-  p.tickets = hd->sk_tickets;
+  p.row_mode = cl.row_split ? 1 : 0;
+  if (!encode_3d_blocks(&mX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, hd->d, B, 64, BN, KB, sw))
+    return cudaErrorInvalidValue;
+  int64_t G;
+  if (p.row_mode) {
+    // G CTAs x tpc tiles of tr_base or tr_base + 1 (<= 128) rows; the first tr_rem tiles are the big
+    // ones.  Boxes of exactly a tile's rows: nothing is read twice or past the tile.
+    G = std::min<int64_t>(hd->num_sms, hd->h);
+    p.tpc = (int)((hd->h + G * 128 - 1) / (G * 128));
+    const int64_t nt = G * p.tpc;
+    p.tr_base = (int)(hd->h / nt);
+    p.tr_rem = (int)(hd->h % nt);
+    const uint32_t rb = (uint32_t)p.tr_base + (p.tr_rem ? 1u : 0u);
+    const uint64_t crow = (uint64_t)hd->d / 32 * NM;
+    if (!encode_2d_bf16(&mW, Wt, hd->d, hd->h, 64, rb, sw) ||
+        !encode_2d_u32(&mC, codes, crow, hd->h, C::CWORDS, rb, code_swizzle(C::CWORDS * 4)) ||
+        !encode_2d_bf16(&mWb, Wt, hd->d, hd->h, 64, (uint32_t)p.tr_base, sw) ||
+        !encode_2d_u32(&mCb, codes, crow, hd->h, C::CWORDS, (uint32_t)p.tr_base, code_swizzle(C::CWORDS * 4)))
+      return cudaErrorInvalidValue;
+    p.units_base = p.units_rem = 0;
+    p.ws = nullptr;
+    p.tickets = nullptr;
+  } else {
+    if (!encode_3d_blocks(&mW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, 128, KB, sw) ||
+        !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, C::CWORDS, 128, code_swizzle(C::CWORDS * 4)))
+      return cudaErrorInvalidValue;
+    mWb = mW;
+    mCb = mC;
+    const int64_t units = (hd->h + 127) / 128 * p.upt;
+    G = std::min<int64_t>(hd->num_sms, units);
+    p.units_base = (int)(units / G);
+    p.units_rem = (int)(units % G);
+    p.tpc = p.tr_base = p.tr_rem = 0;
+    cudaError_t e = sk_workspace(hd, (size_t)hd->num_sms * 2 * C::NOP * BN * 128 * sizeof(float), cl.st);
+    if (e != cudaSuccess) return e;
+    p.ws = hd->sk_ws;
+    p.tickets = hd->sk_tickets;
+  }
+  // one accumulator set (and the TMEM it frees as A slots) when the CTA has a single segment
+  const bool one_seg = p.row_mode && p.tpc == 1;
+  // stage layout: 64-column W blocks of the tile's rows (rounded to the 8-row swizzle atom) and the
+  // code box behind them -- in the row split a stage holds only the tile's rows, so more stages fit
+  if (p.row_mode) {
+    const int rmax = p.tr_base + (p.tr_rem ? 1 : 0);
+    p.wblk = (rmax + 7) / 8 * 1024;
+    p.wsb = (C::KS / 64 * p.wblk + rmax * C::CWORDS * 4 + 1023) / 1024 * 1024;
+  } else {
+    p.wblk = 16384;
+    p.wsb = C::WSB;
+  }
   const size_t cap = (size_t)hd->max_smem_optin;
   p.xstages = 4;
-  const size_t fixed = 1024 + 256 + (size_t)p.xstages * C::XB;   // alignment slack + barriers + x ring
-  if (cap < fixed + 2 * (size_t)C::WSB) return cudaErrorInvalidConfiguration;
-  p.wstages = (int)std::min<size_t>(8, (cap - fixed) / C::WSB);
-  const size_t smem = (size_t)p.wstages * C::WSB + fixed;
-  auto kern = mglu::gemv_tc_kernel<NM, BN, MG>;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(kern, dim3((unsigned)G), dim3(C::THREADS), smem, cl.st, p, mW, mX, mC);
+  const size_t fixed = 1024 + 512 + (size_t)p.xstages * C::XB;   // alignment slack + barriers + x ring
+  if (cap < fixed + 2 * (size_t)p.wsb) return cudaErrorInvalidConfiguration;
+  p.wstages = (int)std::min<size_t>(sk_max_wstages(), (cap - fixed) / p.wsb);
+  const size_t smem = (size_t)p.wstages * p.wsb + fixed;
+  auto kern = one_seg ? mglu::gemv_tc_kernel<NM, BN, MG, true> : mglu::gemv_tc_kernel<NM, BN, MG, false>;
+  // the opt-in shared-memory limit is a per-kernel attribute: set it once (the maximum), not per launch
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [&] {
+    attr_err = cudaFuncSetAttribute(mglu::gemv_tc_kernel<NM, BN, MG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(mglu::gemv_tc_kernel<NM, BN, MG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  return launch_pdl(kern, dim3((unsigned)G), dim3(C::THREADS), smem, cl.st, p, mW, mX, mC, mWb, mCb);
 }
 
 // two masker groups when the TMEM budget allows, else one
@@ -729,7 +803,7 @@ mglu_status mglu_destroy(mglu_handle hd) {
 }
 
 mglu_status mglu_set_path(mglu_handle hd, int path) {
-  if (!hd || path < MGLU_PATH_AUTO || path > MGLU_PATH_TCDEC) return MGLU_ERR_INVALID_ARG;
+  if (!hd || path < MGLU_PATH_AUTO || path > MGLU_PATH_TCROW) return MGLU_ERR_INVALID_ARG;
   std::lock_guard<std::mutex> g(hd->mu);
   hd->path = path;
   return MGLU_OK;
@@ -759,15 +833,18 @@ int mglu_last_path(mglu_handle hd) { return hd ? hd->last_path : -1; }
 // AUTO: the path mglu_forward takes for this handle and batch
 static int auto_path(const mglu_ctx* hd, int64_t B) {
   int path;
-  // measured crossovers at the Llama-3-8B FFN shape (profiles/r02/paths_by_batch.txt): the
-  // register-masked HMMA kernel for B <= 4 (one 8-column MMA tile), the stream-K tcgen05 GEMV for
-  // 5 <= B <= 16, the tcgen05 tile GEMM above; SIMT for fp32 and shapes the others refuse
+  // measured crossovers at the Llama-3-8B FFN shape (profiles/r02/tcrow_sweep.txt): the
+  // register-masked HMMA kernel for B <= 4 (one 8-column MMA tile), the tcgen05 GEMV for
+  // 5 <= B <= 48 on wide layers as its row split (stream-K up to 16 on narrow ones),
+  // the tcgen05 tile GEMM above; SIMT for fp32 and shapes the others refuse
   // (n_m = 8 on large layers: the HMMA kernel's 9 MMAs per step make it compute-bound, and the
-  //  tcgen05 GEMV wins from B = 1: 132 vs 139 us at d=8192 h=28672; on small shards (h < 8192)
-  //  the HMMA kernel stays ahead)
+  //  stream-K tcgen05 GEMV wins from B = 1: 129 vs 138 us at d=8192 h=28672; on small shards
+  //  (h < 8192) the HMMA kernel stays ahead)
   const bool nm8_big = hd->n_m == 8 && hd->h >= 8192 && sk_can_serve(hd, B);
   if (B <= kAutoMmaMaxB && mma_can_serve(hd, B) && !nm8_big)
     path = MGLU_PATH_MMA;
+  else if (B <= kAutoRowMaxB && sk_can_serve(hd, B) && auto_row_split(hd, B))
+    path = MGLU_PATH_TCROW;
   else if (B <= kAutoSkMaxB && sk_can_serve(hd, B))
     path = MGLU_PATH_TCDEC;
   else if (mma_can_serve(hd, B))
@@ -815,13 +892,15 @@ static mglu_status forward_on_path(mglu_handle hd, const void* x, int64_t B, con
     }
     e = tc_nm(hd, x, B, Wt, packed, out, cl);
     launches = 1;
-  } else if (path == MGLU_PATH_TCDEC) {
+  } else if (path == MGLU_PATH_TCDEC || path == MGLU_PATH_TCROW) {
     if (!sk_can_serve(hd, B)) {
       if (prev != hd->device) cudaSetDevice(prev);
       return set_err(hd, MGLU_ERR_UNSUPPORTED,
                      "tcgen05 decode path needs bf16, 1 <= B <= 64 (32 for n_m = 8), d % 64 == 0, d * n_m % 128 == 0");
     }
-    e = sk_nm(hd, x, B, Wt, packed, out, cl);
+    Call c2 = cl;
+    c2.row_split = path == MGLU_PATH_TCROW;
+    e = sk_nm(hd, x, B, Wt, packed, out, c2);
     launches = 1;
   } else {
     if (cl.z)

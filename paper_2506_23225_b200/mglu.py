@@ -24,7 +24,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_PKG_DIR), "include", "mglu.h")
 MGLU_OK, MGLU_ERR_INVALID_ARG, MGLU_ERR_UNSUPPORTED, MGLU_ERR_MISALIGNED, MGLU_ERR_CUDA, MGLU_ERR_OOM = range(6)
 ACT = {"identity": 0, "swish": 1, "gelu": 2, "relu": 3, "sigmoid": 4}
 DTYPE = {"bf16": 0, "f32": 1}
-PATH = {"auto": 0, "simt": 1, "mma": 2, "tcgen05": 3, "tcdec": 4}
+PATH = {"auto": 0, "simt": 1, "mma": 2, "tcgen05": 3, "tcdec": 4, "tcrow": 5}
 TORCH_DTYPE = {"bf16": torch.bfloat16, "f32": torch.float32}
 
 

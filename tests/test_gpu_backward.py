@@ -55,7 +55,7 @@ def test_backward_f32_every_activation(act, n_m):
 
 
 @pytest.mark.parametrize("n_m", [1, 2, 4, 8])
-@pytest.mark.parametrize("path,B", [("auto", 3), ("mma", 2), ("tcdec", 9), ("tcgen05", 40), ("simt", 4)])
+@pytest.mark.parametrize("path,B", [("auto", 3), ("mma", 2), ("tcdec", 9), ("tcrow", 11), ("tcgen05", 40), ("simt", 4)])
 def test_backward_bf16_paths(n_m, path, B):
     if path == "mma" and n_m >= 4 and B > 4:
         pytest.skip("one token group on the MMA path")

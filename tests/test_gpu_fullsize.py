@@ -1,5 +1,5 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (AUTO
-dispatch -> the MMA decode kernel at B = 1, the stream-K tcgen05 GEMV at B = 8), checked on sampled output columns the oracle computes one
+dispatch -> the MMA decode kernel at B = 1, the row-split tcgen05 GEMV at B = 8), checked on sampled output columns the oracle computes one
 by one, plus a one-hot decode probe on sampled k."""
 import numpy as np
 import pytest
@@ -33,7 +33,7 @@ def test_full_size_sampled_columns(name, d, h, n_m, B):
     packed = torch.from_numpy(packed_np).cuda()
     layer = Mglu(d, h, n_m, act="swish", dtype="bf16")
     y = layer.forward(x, Wt, packed).float().cpu().numpy().astype(np.float64)
-    assert layer.last_path() == ("mma" if B <= 4 else "tcdec")     # AUTO crossovers
+    assert layer.last_path() == ("mma" if B <= 4 else "tcrow")     # AUTO crossovers
     rng = np.random.default_rng(1)
     cols = np.unique(np.concatenate([[0, 1, h // 2, h - 2, h - 1], rng.choice(h, 384, replace=False)]))
     xo, Wo = oracle_inputs(inp, "bf16")
@@ -110,7 +110,9 @@ def test_full_size_tensor_core_sampled(name, d, h, n_m, B):
     layer = Mglu(d, h, n_m, act="swish", dtype="bf16")
     y = layer.forward(x, Wt, packed)
     torch.cuda.synchronize()
-    assert layer.last_path() == ("tcdec" if B <= 16 else "tcgen05")
+    wide = h >= torch.cuda.get_device_properties(0).multi_processor_count * 64
+    want = "tcrow" if (5 <= B <= 48 and n_m <= 4 and wide) else ("tcdec" if B <= 16 else "tcgen05")
+    assert layer.last_path() == want                               # AUTO crossovers
     rng = np.random.default_rng(B + n_m)
     toks = np.unique(np.concatenate([[0, B - 1], rng.choice(B, min(B, 46), replace=False)]))
     cols = np.unique(np.concatenate([[0, 127, 128, h - 1], rng.choice(h, 92, replace=False)]))

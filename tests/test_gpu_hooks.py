@@ -30,7 +30,7 @@ def _one_hot_probe(layer, Wt, packed, d, T):
     return np.concatenate(out)                            # [d][h]
 
 
-@pytest.mark.parametrize("path,T", [("mma", 4), ("tcdec", 8), ("tcgen05", 32), ("simt", 8)])
+@pytest.mark.parametrize("path,T", [("mma", 4), ("tcdec", 8), ("tcrow", 16), ("tcgen05", 32), ("simt", 8)])
 def test_mask_corruption_hook_is_detected(path, T):
     from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
     d, h, n_m = 256, 200, 4

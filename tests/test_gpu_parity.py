@@ -106,7 +106,7 @@ def test_partials_vs_independent_value_stream(n_m, dtype):
 
 
 @pytest.mark.parametrize("n_m", [1, 2, 4, 8])
-@pytest.mark.parametrize("path,B", [("mma", 1), ("mma", 3), ("tcdec", 1), ("tcdec", 9), ("tcgen05", 2), ("tcgen05", 70)])
+@pytest.mark.parametrize("path,B", [("mma", 1), ("mma", 3), ("tcdec", 1), ("tcdec", 9), ("tcrow", 1), ("tcrow", 17), ("tcgen05", 2), ("tcgen05", 70)])
 def test_fast_path_partials_vs_independent_value_stream(n_m, path, B):
     """The fast kernels' own value streams (each kernel's epilogue writes s_i = (t + u_i) / 2 and
     t - s_i instead of y when the partials entry selects it): checked against the oracle's gate and

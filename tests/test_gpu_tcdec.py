@@ -141,3 +141,65 @@ def test_tcdec_matches_mma_path_sampled_full_size():
         o = oracle()
         ref = o.forward(xo, Wo[cols], cols, o.pack(inp["bits"]), n_m, 1)
         assert normwise_err(y[:, cols], ref) <= TIGHT["bf16"]
+
+
+# row split (MGLU_PATH_TCROW): every CTA owns whole tiles of tr_base or tr_base + 1 rows over all of d
+ROW_SHAPES = [  # (d, h, B)
+    (4096, 9472, 1),     # exactly 64 rows per CTA
+    (1024, 9601, 5),     # 64 / 65-row tiles (two TMA box heights)
+    (512, 19000, 24),    # two tiles per CTA, 64 / 65 rows
+    (2048, 14336, 40),   # the config-3 split (96 / 97 rows), BN = 64, ragged tokens
+    (256, 38000, 64),    # three tiles per CTA, full token tile
+]
+
+
+@pytest.mark.parametrize("n_m", [1, 2, 4, 8])
+@pytest.mark.parametrize("d,h,B", ROW_SHAPES)
+def test_tcdec_row_split_shapes(n_m, d, h, B):
+    from paper_2506_23225_b200.mglu import MgluError, MGLU_ERR_UNSUPPORTED
+    inp = make_inputs(9100 + 13 * n_m + d + h + B, B=B, d=d, h=h, n_m=n_m, dtype="bf16")
+    if n_m == 8 and B > 32:
+        with pytest.raises(MgluError) as e:
+            gpu_forward(inp, "bf16", n_m, "swish", path="tcrow")
+        assert e.value.status == MGLU_ERR_UNSUPPORTED
+        return
+    y, used = gpu_forward(inp, "bf16", n_m, "swish", path="tcrow")
+    assert used == "tcrow"
+    rng = np.random.default_rng(h + B)
+    cols = np.unique(np.concatenate([[0, 63, 64, 65, 96, 97, h // 2, h - 2, h - 1], rng.choice(h, 300, replace=False)]))
+    ref = oracle_forward(inp, "bf16", n_m, "swish", cols=cols)
+    assert normwise_err(y[:, cols], ref) <= TIGHT["bf16"]
+
+
+@pytest.mark.parametrize("n_m", [1, 4, 8])
+def test_tcdec_row_split_one_hot_bit_exact(n_m):
+    """The one-hot decode probe through the row split (MGLU_PATH_TCROW): every (row, column) of a layer with 64- and
+    65-row tiles, bit-exact."""
+    from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
+    d, h = 256, 9601
+    inp = make_inputs(171 + n_m, B=1, d=d, h=h, n_m=n_m, dtype="bf16")
+    bits = inp["bits"]
+    packed = torch.from_numpy(mglu_pack_masks_host(bits)).cuda()
+    Wt = torch.ones(h, d, device="cuda", dtype=torch.bfloat16)
+    eye = torch.eye(d, device="cuda", dtype=torch.bfloat16)
+    layer = Mglu(d, h, n_m, act="sigmoid", dtype="bf16", path="tcrow")
+    want = (n_m - bits.sum(axis=0).T) / 2.0                        # [d][h]
+    for k0 in range(0, d, 16):
+        y = layer.forward(eye[k0:k0 + 16].contiguous(), Wt, packed).float().cpu().numpy()
+        np.testing.assert_array_equal(y, want[k0:k0 + 16])
+
+
+def test_tcdec_row_split_shard_bit_identical():
+    """P8 on the row split: a row's k-order does not depend on which CTA or tile holds it, so an
+    h-shard (pointer offsets into Wt and the codes) reproduces the unsharded output bit for bit."""
+    from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host
+    d, h, n_m, B = 2048, 19200, 4, 8
+    inp = make_inputs(44, B=B, d=d, h=h, n_m=n_m, dtype="bf16")
+    x, Wt = to_device(inp, "bf16")
+    packed = torch.from_numpy(mglu_pack_masks_host(inp["bits"])).cuda()
+    full = Mglu(d, h, n_m, act="swish", dtype="bf16", path="tcrow").forward(x, Wt, packed)
+    row_bytes = d * n_m // 8
+    for lo, hi in ((0, 9600), (9600, 19200), (4800, 14400)):
+        part = Mglu(d, hi - lo, n_m, act="swish", dtype="bf16", path="tcrow")
+        y = part.forward(x, Wt[lo:hi], packed[lo * row_bytes:hi * row_bytes])
+        assert torch.equal(y, full[:, lo:hi]), (lo, hi)

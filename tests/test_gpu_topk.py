@@ -98,7 +98,7 @@ def test_router_matches_oracle(n_m, K, B):
     assert np.allclose(G.sum(axis=1), 1.0, atol=1e-6)
 
 
-@pytest.mark.parametrize("path", ["mma", "simt", "tcdec", "tcgen05"])
+@pytest.mark.parametrize("path", ["mma", "simt", "tcdec", "tcrow", "tcgen05"])
 @pytest.mark.parametrize("n_m,K,B", [(4, 1, 1), (4, 2, 3), (8, 2, 1), (8, 3, 5), (8, 8, 8), (2, 1, 2), (8, 1, 2),
                                      (8, 4, 1), (8, 2, 2)])
 def test_routed_forward_matches_oracle(path, n_m, K, B):

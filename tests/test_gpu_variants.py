@@ -30,7 +30,7 @@ def _oracle_variant(inp, n_m, act_code, variant):
 
 @pytest.mark.parametrize("variant", ["no_gate_mask", "no_value_mask", "no_masks"])
 @pytest.mark.parametrize("n_m,B,path", [(1, 1, "mma"), (4, 3, "mma"), (1, 10, "auto"), (2, 2, "simt"),
-                                         (4, 7, "tcdec"), (1, 100, "tcgen05"), (8, 70, "tcgen05")])
+                                         (4, 7, "tcdec"), (2, 12, "tcrow"), (1, 100, "tcgen05"), (8, 70, "tcgen05")])
 def test_variant_matches_oracle(variant, n_m, B, path):
     from oracle import VARIANTS
     from paper_2506_23225_b200.mglu import Mglu, mglu_pack_masks_host

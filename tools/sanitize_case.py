@@ -19,7 +19,7 @@ def main():
         packed = mglu_pack_masks_device(bits)
         assert torch.equal(mglu_unpack_masks_device(packed, n_m, h, d), bits)
         Wt = (torch.randn(h, d, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
-        for path, B in (("mma", 3), ("tcdec", 9), ("tcgen05", 40), ("simt", 2)):
+        for path, B in (("mma", 3), ("tcdec", 9), ("tcrow", 12), ("tcgen05", 40), ("simt", 2)):
             if path == "mma" and n_m >= 4 and B > 4:
                 continue
             x = torch.randn(B, d, device="cuda", generator=g).to(torch.bfloat16)
