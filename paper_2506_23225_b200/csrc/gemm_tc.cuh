@@ -42,6 +42,9 @@ template <> struct TcCfg<2> { static constexpr int BN = 128, KA = 32, MPC = 2; }
 #endif
 template <> struct TcCfg<4> { static constexpr int BN = MGLU_TC_BN4, KA = MGLU_TC_KA4, MPC = 4; };
 template <> struct TcCfg<8> { static constexpr int BN = 64, KA = 32, MPC = 4; };
+// n_m = 16: a cluster of four CTAs, four masks each; 32-token tiles keep
+// the three partner buffers of the DSMEM reduction beside a 4-stage ring
+template <> struct TcCfg<16> { static constexpr int BN = 32, KA = 32, MPC = 4; };
 
 constexpr int kTcThreads = 320;
 constexpr int kTcMaskWarps = 8;
@@ -66,13 +69,13 @@ template <int NM, int BN> __host__ __device__ constexpr int tc_stage_bytes() {
   return tc_x_bytes<BN>() + 128 * kTcK * 2 + 128 * tc_code_words<NM>() * 4;
 }
 template <int NM> __host__ __device__ constexpr int tc_split() { return NM / TcCfg<NM>::MPC; }
-// DSMEM buffer of the mask-split reduction: the partner's fp32 partial outputs [BN][128]
-template <int NM, int BN> __host__ __device__ constexpr int tc_red_bytes() { return tc_split<NM>() > 1 ? BN * 128 * 4 : 0; }
+// DSMEM buffers of the mask-split reduction on cluster rank 0: each partner's fp32 partial outputs [BN][128]
+template <int NM, int BN> __host__ __device__ constexpr int tc_red_bytes() { return (tc_split<NM>() - 1) * BN * 128 * 4; }
 template <int NM> __host__ __device__ constexpr int tc_tmem_used() {
   return (TcCfg<NM>::MPC + 1) * TcCfg<NM>::BN + 2 * (TcCfg<NM>::MPC + 1) * TcCfg<NM>::KA / 2;
 }
 static_assert(tc_tmem_used<1>() <= 512 && tc_tmem_used<2>() <= 512 && tc_tmem_used<4>() <= 512 &&
-              tc_tmem_used<8>() <= 512, "TMEM budget");
+              tc_tmem_used<8>() <= 512 && tc_tmem_used<16>() <= 512, "TMEM budget");
 
 struct TcParams {
   __nv_bfloat16* out;        // [B][h]
@@ -311,9 +314,10 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
         yp[ch][q] = acc;
       }
       if constexpr (NSPLIT > 1) {
-        if (blockIdx.z == 1) {                             // partial of masks 5..8 -> rank 0's buffer
+        if (blockIdx.z > 0) {                              // partial of this rank's masks -> rank 0's buffer
+          float* rb = red + (size_t)(blockIdx.z - 1) * BN * 128;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) st_cluster_f32(red + (c0 + q) * 128 + m, 0, yp[ch][q]);
+          for (int q = 0; q < 8; ++q) st_cluster_f32(rb + (c0 + q) * 128 + m, 0, yp[ch][q]);
         }
       } else {
         const int grow = m0 + m;
@@ -343,7 +347,8 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
         for (int q = 0; q < 8; ++q) {
           const int tok = n0 + c0 + q;
           float y = yp[ch][q];
-          if constexpr (NSPLIT > 1) y += red[(c0 + q) * 128 + m];        // masks 1..4 + masks 5..8
+#pragma unroll
+          for (int r = 1; r < NSPLIT; ++r) y += red[(size_t)(r - 1) * BN * 128 + (c0 + q) * 128 + m];   // rank order
           if (tok < p.B) p.out[(size_t)tok * p.h + grow] = __float2bfloat16_rn(y);
         }
       }

@@ -389,7 +389,7 @@ cudaError_t mma_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const voi
 // ------------------------------------------------------------------ tcgen05 (prefill) dispatch
 bool tc_can_serve(const mglu_ctx* hd, int64_t B) {
   // TMA of the mask words: rows of d/32 * n_m u32 words must be 16-byte multiples
-  return hd->dtype == MGLU_BF16 && fast_nm(hd->n_m) && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 &&
+  return hd->dtype == MGLU_BF16 && (fast_nm(hd->n_m) || hd->n_m == 16) && (hd->d / 32 * hd->n_m) % 4 == 0 && B >= 1 &&
          B <= ((int64_t)1 << 31) - 1;
 }
 
@@ -470,7 +470,7 @@ cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
-  at[1].id = cudaLaunchAttributeClusterDimension;          // mask-split pair (n_m = 8) shares DSMEM
+  at[1].id = cudaLaunchAttributeClusterDimension;          // mask-split CTAs (n_m = 8: 2, 16: 4) share DSMEM
   at[1].val.clusterDim.x = 1;
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = NSPLIT;
@@ -486,8 +486,11 @@ cudaError_t run_tc(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const
                    const Call& cl) {
   if (B <= 16) return run_tc_bn<NM, ACT, 16>(hd, x, B, Wt, codes, out, cl);
   if (B <= 32) return run_tc_bn<NM, ACT, 32>(hd, x, B, Wt, codes, out, cl);
-  if (B <= 64 || mglu::TcCfg<NM>::BN == 64) return run_tc_bn<NM, ACT, 64>(hd, x, B, Wt, codes, out, cl);
-  return run_tc_bn<NM, ACT, mglu::TcCfg<NM>::BN>(hd, x, B, Wt, codes, out, cl);
+  if constexpr (mglu::TcCfg<NM>::BN <= 32) return run_tc_bn<NM, ACT, 32>(hd, x, B, Wt, codes, out, cl);
+  else {
+    if (B <= 64 || mglu::TcCfg<NM>::BN == 64) return run_tc_bn<NM, ACT, 64>(hd, x, B, Wt, codes, out, cl);
+    return run_tc_bn<NM, ACT, mglu::TcCfg<NM>::BN>(hd, x, B, Wt, codes, out, cl);
+  }
 }
 
 template <int NM>
@@ -508,7 +511,9 @@ cudaError_t tc_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const 
     case 1: return tc_act<1>(hd, x, B, Wt, codes, out, cl);
     case 2: return tc_act<2>(hd, x, B, Wt, codes, out, cl);
     case 4: return tc_act<4>(hd, x, B, Wt, codes, out, cl);
-    default: return tc_act<8>(hd, x, B, Wt, codes, out, cl);
+    case 8: return tc_act<8>(hd, x, B, Wt, codes, out, cl);
+    case 16: return tc_act<16>(hd, x, B, Wt, codes, out, cl);
+    default: return cudaErrorInvalidValue;
   }
 }
 
