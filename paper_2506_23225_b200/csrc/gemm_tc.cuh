@@ -31,17 +31,19 @@ namespace mglu {
 template <int NM> struct TcCfg;
 template <> struct TcCfg<1> { static constexpr int BN = 224, KA = 32, MPC = 1; };
 template <> struct TcCfg<2> { static constexpr int BN = 128, KA = 32, MPC = 2; };
-#ifndef MGLU_TC_KA4
-#define MGLU_TC_KA4 32
-#endif
+
 #ifndef MGLU_TC_ODD_SLOTS
 #define MGLU_TC_ODD_SLOTS 0
 #endif
+// n_m = 4 (and each CTA of the n_m = 8 pair): 80-token tiles with 16-column A-stages -- five
+// accumulators of 80 columns leave two 40-column A slots; the tensor work per masked operand is 25 %
+// larger than at 64 tokens with 32-column stages (2 slots of 80): config 4 8.12 vs 9.07 ms
+// (profiles/r02/prefill_tiles.txt)
 #ifndef MGLU_TC_BN4
-#define MGLU_TC_BN4 64
+#define MGLU_TC_BN4 80
 #endif
-template <> struct TcCfg<4> { static constexpr int BN = MGLU_TC_BN4, KA = MGLU_TC_KA4, MPC = 4; };
-template <> struct TcCfg<8> { static constexpr int BN = 64, KA = 32, MPC = 4; };
+template <> struct TcCfg<4> { static constexpr int BN = MGLU_TC_BN4, KA = 32, MPC = 4; };
+template <> struct TcCfg<8> { static constexpr int BN = MGLU_TC_BN4, KA = 32, MPC = 4; };
 // n_m = 16: a cluster of four CTAs, four masks each; 32-token tiles keep
 // the three partner buffers of the DSMEM reduction beside a 4-stage ring
 template <> struct TcCfg<16> { static constexpr int BN = 32, KA = 32, MPC = 4; };
@@ -55,8 +57,12 @@ constexpr int kTcK = 64;                        // reduction columns per shared 
 #define MGLU_TC_SS_T 0   // 1: t's MMA reads W straight from shared memory (SS); slots hold the masked copies only
 #endif
 template <int NM> __host__ __device__ constexpr int tc_slot_ops() { return TcCfg<NM>::MPC + (MGLU_TC_SS_T ? 0 : 1); }
+// A-stage width of a BN-token tile: 32 columns when two such slots fit beside the accumulators, else 16
+template <int NM, int BN> __host__ __device__ constexpr int tc_ka() {
+  return (TcCfg<NM>::MPC + 1) * BN + 2 * tc_slot_ops<NM>() * TcCfg<NM>::KA / 2 <= 512 ? TcCfg<NM>::KA : 16;
+}
 template <int NM, int BN> __host__ __device__ constexpr int tc_slots() {
-  constexpr int acc = (TcCfg<NM>::MPC + 1) * BN, slot = tc_slot_ops<NM>() * TcCfg<NM>::KA / 2;
+  constexpr int acc = (TcCfg<NM>::MPC + 1) * BN, slot = tc_slot_ops<NM>() * tc_ka<NM, BN>() / 2;
   constexpr int fit = (512 - acc) / slot;
   return fit >= 4 ? 4 : (MGLU_TC_ODD_SLOTS && fit == 3) ? 3 : 2;
 }
@@ -72,7 +78,7 @@ template <int NM> __host__ __device__ constexpr int tc_split() { return NM / TcC
 // DSMEM buffers of the mask-split reduction on cluster rank 0: each partner's fp32 partial outputs [BN][128]
 template <int NM, int BN> __host__ __device__ constexpr int tc_red_bytes() { return (tc_split<NM>() - 1) * BN * 128 * 4; }
 template <int NM> __host__ __device__ constexpr int tc_tmem_used() {
-  return (TcCfg<NM>::MPC + 1) * TcCfg<NM>::BN + 2 * (TcCfg<NM>::MPC + 1) * TcCfg<NM>::KA / 2;
+  return (TcCfg<NM>::MPC + 1) * TcCfg<NM>::BN + 2 * (TcCfg<NM>::MPC + 1) * tc_ka<NM, TcCfg<NM>::BN>() / 2;
 }
 static_assert(tc_tmem_used<1>() <= 512 && tc_tmem_used<2>() <= 512 && tc_tmem_used<4>() <= 512 &&
               tc_tmem_used<8>() <= 512 && tc_tmem_used<16>() <= 512, "TMEM budget");
@@ -91,7 +97,7 @@ template <int NM, int ACT, int BN>
 __global__ void __launch_bounds__(kTcThreads, 1)
 gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mW,
                const __grid_constant__ CUtensorMap mC) {
-  constexpr int KA = TcCfg<NM>::KA, SA = tc_slots<NM, BN>();
+  constexpr int KA = tc_ka<NM, BN>(), SA = tc_slots<NM, BN>();
   constexpr int NSL = tc_slot_ops<NM>();                  // operands stored per A slot
   constexpr int SS = MGLU_TC_SS_T;                         // t from shared memory
   static_assert((TcCfg<NM>::MPC + 1) * BN + SA * NSL * KA / 2 <= 512, "TMEM budget");
