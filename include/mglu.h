@@ -160,6 +160,13 @@ mglu_status mglu_router_topk(mglu_handle hd, const void* x, int64_t B, const voi
 mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* packed,
                                 const float* G, int K, void* out, void* stream);
 
+/* Top-K routed forward on PLANE-MAJOR codes (mglu_pack_planes_*): the same result as
+ * mglu_forward_routed on the interleaved codes (bit-identical: same kernel arithmetic), but each
+ * stage streams W and only the planes some token selected.  MMA path only: bf16, Swish, standard
+ * variant, 1 <= B <= 4, d % 128 == 0, 1 <= K <= n_m; other configurations return UNSUPPORTED. */
+mglu_status mglu_forward_routed_planes(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* planes,
+                                       const float* G, int K, void* out, void* stream);
+
 /* End-to-end form: x_host [B][d] and out_host [B][h] are HOST buffers (pinned for async
  * copies; pageable works but serialises).  Copies x to the handle's device staging buffer,
  * runs mglu_forward, copies y back, all enqueued on `stream` (the caller synchronises).  The
@@ -186,6 +193,15 @@ mglu_status mglu_pack_logits_host(const float* logits, int n_m, int64_t h, int64
                                   uint8_t* packed);
 mglu_status mglu_unpack_masks_host(const uint8_t* packed, int n_m, int64_t h, int64_t d,
                                    uint8_t* bits);
+/* Plane-major code layout (row f2): plane i (mask i + 1) is [h][d/32] u32 words, word
+ * (i, j, g) at byte offset ((i h + j) d/32 + g) * 4, each word holding M_{i+1}[j, 32g .. 32g+31] in
+ * the same pair-split bit order as the interleaved layout (R3).  Same h*d*n_m/8 bytes; a routed
+ * call on it loads only the planes its tokens selected (16 + K instead of 16 + n_m bits per
+ * element).  These convert an interleaved `packed` (mglu_pack_masks_*) into `planes`.
+ * Errors: INVALID_ARG (null / negative), UNSUPPORTED (n_m, d % 32), MISALIGNED (device). */
+mglu_status mglu_pack_planes_host(const uint8_t* packed, int n_m, int64_t h, int64_t d, uint8_t* planes);
+mglu_status mglu_pack_planes_device(const uint8_t* packed, int n_m, int64_t h, int64_t d, uint8_t* planes,
+                                    void* stream);
 mglu_status mglu_pack_masks_device(const uint8_t* bits, int n_m, int64_t h, int64_t d,
                                    uint8_t* packed, void* stream);
 mglu_status mglu_pack_logits_device(const float* logits, int n_m, int64_t h, int64_t d,

@@ -50,6 +50,12 @@ constexpr int kDecWBytes = kDecConsumers * 2048;       // W region of a stage sl
 template <int NM> __host__ __device__ constexpr int dec_code_span() { return 16 * NM; }   // 0: dense (n_m = 0)
 // stage slot = W region + codes region (16384 elements: 128 row-blocks x 16 n_m bytes)
 template <int NM> __host__ __device__ constexpr int dec_stage_bytes() { return kDecWBytes + 128 * kDecConsumers * NM; }
+// plane-major codes (routed, row f2): a stage holds W and the KSEL selected planes' words only
+// (16384 elements x 1 bit = 2 KB per plane)
+constexpr int kDecPlaneBytes = 2048;
+template <int NM, int KSEL, bool PL> __host__ __device__ constexpr int dec_stage_bytes_pl() {
+  return PL ? kDecWBytes + KSEL * kDecPlaneBytes : dec_stage_bytes<NM>();
+}
 
 struct DecParams {
   const __nv_bfloat16* x;
@@ -74,6 +80,22 @@ struct DecMaps {
   CUtensorMap w[4];
   CUtensorMap c[4];
 };
+
+// Top-K routed forward: the masks some token of the batch selected (nonzero G), at most KSEL of
+// them, lowest index first, in slots 0..nsel-1; unused slots repeat slot 0 (static register
+// indexing: __fns finds the bit, no local-memory array)
+template <int NM, int KSEL>
+__device__ __forceinline__ int dec_select(const float* G, int B, int (&sel)[KSEL]) {
+  uint32_t active = 0u;
+  for (int q = 0; q < B * NM; ++q) active |= (G[q] != 0.0f ? 1u : 0u) << (q % NM);
+  const int nsel = min(__popc(active), KSEL);
+#pragma unroll
+  for (int k = 0; k < KSEL; ++k) sel[k] = k < nsel ? (int)__fns(active, 0, k + 1) : 0;
+#pragma unroll
+  for (int k = 0; k < KSEL; ++k)
+    if (k >= nsel) sel[k] = sel[0];
+  return nsel;
+}
 
 // swizzled byte offset within a 1024-aligned region of `rb`-byte rows (rb in {16..128})
 __device__ __forceinline__ uint32_t swz(uint32_t lin, uint32_t rb) {
@@ -108,11 +130,17 @@ __device__ __forceinline__ void dec_stage_of(int i, int nfull, int rem, int d, i
   }
 }
 
-template <int NM, int ACT, int NB, int KSEL>
+// PL (routed only, KSEL > 0): the codes are PLANE-MAJOR -- plane i is [h][d/32] words, the same
+// pair-split bit order within a word (mglu_pack_planes_*) -- and a stage loads only the planes the
+// batch selected, so a routed call reads W plus K (not n_m) bits per element (row f2).
+// maps.c[ti] then views the planes as one [n_m h][d/32] word tensor with boxes of 8T rows x KS/32
+// words; the selection needs G, so this producer starts after griddepcontrol.wait.
+template <int NM, int ACT, int NB, int KSEL, bool PL = false>
 __global__ void __launch_bounds__(kDecThreads, 1)
 gemv_mma_kernel(const DecParams p, const __grid_constant__ DecMaps maps) {
+  static_assert(!PL || KSEL > 0, "plane-major codes: routed calls only");
   constexpr int SPAN = dec_code_span<NM>();
-  constexpr int SB = dec_stage_bytes<NM>();
+  constexpr int SB = dec_stage_bytes_pl<NM, KSEL, PL>();
   constexpr int NACC = NB * ((KSEL > 0 ? KSEL : NM) + 1);
   // 32-column steps loaded per register group: all 4 of a stage, or 2 / 1 where the staged
   // operands would not fit beside the accumulators (n_m = 8; two token groups with n_m >= 4).
@@ -163,14 +191,52 @@ gemv_mma_kernel(const DecParams p, const __grid_constant__ DecMaps maps) {
         if (NM > 0) prefetch_tmap(&maps.c[t]);
       }
       const uint64_t pol = policy_evict_first();
+      int psel[PL ? KSEL : 1];
+      int pn = 0;
+      if constexpr (PL) {
+        // the ring's first stages of W (constant weights) stream before the PDL wait: their
+        // barriers expect the W bytes now, the selected planes' bytes and the arrival after it
+        const int pre = min(S, nstages);
+        for (int i = 0; i < pre; ++i) {
+          int ti, row0, ks;
+          dec_stage_of(i, nfull, rem, d, ti, row0, ks);
+          mbar_expect_tx(&full[i], (uint32_t)(16384 * 2));
+          tma_load_3d_hint(ring + (size_t)i * SB, &maps.w[ti], 0, r0 + row0, ks * (256 << ti) / 64, &full[i], pol);
+        }
+        pdl_wait();                                          // G comes from the router launch
+        pn = dec_select<NM, KSEL>(p.G, p.B, psel);
+        for (int i = 0; i < pre; ++i) {
+          int ti, row0, ks;
+          dec_stage_of(i, nfull, rem, d, ti, row0, ks);
+          mbar_arrive_expect_tx(&full[i], (uint32_t)(pn * kDecPlaneBytes));
+#pragma unroll
+          for (int k = 0; k < KSEL; ++k)
+            if (k < pn) tma_load_2d_hint(ring + (size_t)i * SB + kDecWBytes + k * kDecPlaneBytes, &maps.c[ti],
+                                         ks * (256 << ti) / 32, psel[k] * p.h + r0 + row0, &full[i], pol);
+        }
+      }
       int s = 0;
       uint32_t ph = 0;
       for (int i = 0; i < nstages; ++i) {
         int ti, row0, ks;
         dec_stage_of(i, nfull, rem, d, ti, row0, ks);
         const int k0 = ks * (256 << ti);
+        if constexpr (PL) {
+          if (i < S) { if (++s == S) { s = 0; ph ^= 1; } continue; }   // issued above
+        }
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* wst = ring + (size_t)s * SB;
+        if constexpr (PL) {
+          // W + the selected planes' words of the stage's rows (8T rows x KS/32 words each)
+          mbar_arrive_expect_tx(&full[s], (uint32_t)(16384 * 2 + pn * kDecPlaneBytes));
+          tma_load_3d_hint(wst, &maps.w[ti], 0, r0 + row0, k0 / 64, &full[s], pol);
+#pragma unroll
+          for (int k = 0; k < KSEL; ++k)
+            if (k < pn) tma_load_2d_hint(wst + kDecWBytes + k * kDecPlaneBytes, &maps.c[ti], k0 / 32,
+                                         psel[k] * p.h + r0 + row0, &full[s], pol);
+          if (++s == S) { s = 0; ph ^= 1; }
+          continue;
+        }
         mbar_arrive_expect_tx(&full[s], (uint32_t)(16384 * 2 + 16384 / 128 * SPAN));
         tma_load_3d_hint(wst, &maps.w[ti], 0, r0 + row0, k0 / 64, &full[s], pol);
         if constexpr (NM > 0) tma_load_3d_hint(wst + kDecWBytes, &maps.c[ti], 0, r0 + row0, k0 / 128, &full[s], pol);
@@ -251,18 +317,10 @@ gemv_mma_kernel(const DecParams p, const __grid_constant__ DecMaps maps) {
   uint32_t valid = (1u << NSLOT) - 1u;
 #pragma unroll
   for (int k = 0; k < NSLOT; ++k) sel[k] = k;
+  int nsel = NSLOT;
   if constexpr (KSEL > 0) {
-    uint32_t active = 0u;
-    for (int q = 0; q < B * NM; ++q) active |= (p.G[q] != 0.0f ? 1u : 0u) << (q % NM);
-    // slot k = the (k+1)-th selected mask, lowest index first (static register indexing: __fns
-    // finds the bit, no local-memory array)
-    const int nsel = min(__popc(active), KSEL);
+    nsel = dec_select<NM, KSEL>(p.G, B, sel);
     valid = (1u << nsel) - 1u;
-#pragma unroll
-    for (int k = 0; k < NSLOT; ++k) sel[k] = k < nsel ? (int)__fns(active, 0, k + 1) : 0;
-#pragma unroll
-    for (int k = 0; k < NSLOT; ++k)
-      if (k >= nsel) sel[k] = sel[0];
   }
   named_bar_sync(1, kDecConsumers * 32);
 
@@ -305,7 +363,14 @@ gemv_mma_kernel(const DecParams p, const __grid_constant__ DecMaps maps) {
     }
     // routed: the selected masks' words (one 4-byte read per slot and step)
     uint32_t csel[KSEL > 0 ? KSEL : 1][4];
-    if constexpr (KSEL > 0) {
+    if constexpr (PL) {
+      // plane box of slot k (slots past nsel reuse slot 0's plane): row srow, word kp * 4 + st
+#pragma unroll
+      for (int k = 0; k < KSEL; ++k)
+#pragma unroll
+        for (int st = 0; st < 4; ++st)
+          csel[k][st] = (uint32_t)(kDecWBytes + (k < nsel ? k : 0) * kDecPlaneBytes + srow * (32 << ti) + (kp * 4 + st) * 4);
+    } else if constexpr (KSEL > 0) {
 #pragma unroll
       for (int k = 0; k < KSEL; ++k)
 #pragma unroll

@@ -48,6 +48,7 @@ struct mglu_ctx {
     bool valid = false;
     const void* Wt = nullptr;
     const void* codes = nullptr;
+    bool planes = false;           // codes in the plane-major layout (routed, row f2)
     uint64_t stamp = 0;
     mglu::DecMaps maps;
   };
@@ -73,6 +74,7 @@ struct Call {
   int K = 0;                  // K of the routed call (0: unknown -> every mask evaluated)
   float* z = nullptr;         // mglu_forward_partials: Alg. 1's z [B][2 n_m][h] instead of y
   bool row_split = false;     // tcgen05 GEMV: row split (MGLU_PATH_TCROW) instead of stream-K
+  bool planes = false;        // routed call with plane-major codes (mglu_forward_routed_planes)
 };
 
 const char* kStatusStr[] = {"MGLU_OK", "MGLU_ERR_INVALID_ARG", "MGLU_ERR_UNSUPPORTED",
@@ -208,10 +210,10 @@ bool encode_3d_blocks(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, cons
 // descriptor cache keyed by (Wt, codes).  W: 64-column blocks (SW128); codes: 128-column blocks of
 // 16*n_m bytes (swizzle = span).  Round type ti (T = 8 >> ti tiles): boxes of 8T rows x
 // (2 WPT | WPT) blocks, WPT = 2 << ti.
-bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, mglu::DecMaps* out) {
+bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, mglu::DecMaps* out, bool planes = false) {
   std::lock_guard<std::mutex> g(hd->mu);
   for (auto& e : hd->dec_cache)
-    if (e.valid && e.Wt == Wt && e.codes == codes) {
+    if (e.valid && e.Wt == Wt && e.codes == codes && e.planes == planes) {
       e.stamp = ++hd->dec_clock;
       *out = e.maps;
       return true;
@@ -227,7 +229,18 @@ bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, mglu::DecMaps* ou
     if (!encode_3d_blocks(&m.w[ti], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, rows, 2 * wpt, sw))
       return false;
     if (NM == 0) m.c[ti] = m.w[ti];                          // dense projection: W boxes only
-    else if (!encode_3d_blocks(&m.c[ti], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, rows, wpt, csw))
+    else if (planes) {
+      // plane-major codes: one [n_m h][d/32] u32 tensor, boxes of 8T rows x KS/32 words
+      EncodeTiledFn enc = get_encoder();
+      cuuint64_t dims[2] = {(cuuint64_t)hd->d / 32, (cuuint64_t)(NM * hd->h)};
+      cuuint64_t strides[1] = {(cuuint64_t)hd->d / 32 * 4};
+      cuuint32_t box[2] = {8u << ti, rows};
+      cuuint32_t es[2] = {1, 1};
+      if (!enc || enc(&m.c[ti], CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(codes), dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    } else if (!encode_3d_blocks(&m.c[ti], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, codes, crow_u32, hd->h, span / 4, rows, wpt, csw))
       return false;
   }
   size_t victim = 0;
@@ -236,7 +249,7 @@ bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, mglu::DecMaps* ou
     if (hd->dec_cache[i].stamp < hd->dec_cache[victim].stamp) victim = i;
   }
   auto& e = hd->dec_cache[victim];
-  e.valid = true; e.Wt = Wt; e.codes = codes; e.stamp = ++hd->dec_clock;
+  e.valid = true; e.Wt = Wt; e.codes = codes; e.planes = planes; e.stamp = ++hd->dec_clock;
   e.maps = m;
   *out = m;
   return true;
@@ -273,7 +286,7 @@ int dec_l2pf() {
   return v;
 }
 
-template <int NM, int ACT, int NB, int KSEL>
+template <int NM, int ACT, int NB, int KSEL, bool PL = false>
 cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
                        void* out, const Call& cl) {
   mglu::DecParams p;
@@ -294,7 +307,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   p.l2pf = dec_l2pf();
   p.light_drop = 0;
   mglu::DecMaps maps;
-  if (!dec_maps(hd, Wt, codes, &maps)) return cudaErrorInvalidValue;
+  if (!dec_maps(hd, Wt, codes, &maps, PL)) return cudaErrorInvalidValue;
   // x in smem, split by pair parity and zero-padded to the last column any stage can touch (the
   // widest round type a CTA of this grid runs)
   int64_t maxcol = hd->d;
@@ -308,7 +321,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   }
   const int npair = (int)(maxcol / 2);
   p.xpar = npair / 2 + 8;
-  constexpr size_t SB = mglu::dec_stage_bytes<NM>();
+  constexpr size_t SB = mglu::dec_stage_bytes_pl<NM, KSEL, PL>();
   const size_t xbytes = (size_t)2 * B * p.xpar * 4;
   const size_t partbytes = (size_t)mglu::kDecConsumers * 32 * NB * ((KSEL > 0 ? KSEL : NM) + 1) * 4;
   const size_t fixed = xbytes + partbytes + 1024;
@@ -326,7 +339,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
     p.light_drop = 1;
   }
   const size_t smem = (size_t)p.stages * SB + 2 * p.stages * sizeof(uint64_t) + partbytes + xbytes;
-  auto kern = mglu::gemv_mma_kernel<NM, ACT, NB, KSEL>;
+  auto kern = mglu::gemv_mma_kernel<NM, ACT, NB, KSEL, PL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(kern, dim3((unsigned)ncta), dim3(mglu::kDecThreads), smem, cl.st, p, maps);
@@ -338,6 +351,20 @@ cudaError_t run_mma(mglu_ctx* hd, const void* x, int B, const void* Wt, const vo
   // routed (Top-K) swish forward: evaluate only the masks some token selected -- at most K per
   // token, so min(n_m, B*K) slots, rounded up to a power of two (other activations and larger
   // unions run all masks with the weights in the epilogue)
+  if (cl.planes) {
+    // plane-major codes: routed Swish calls of B <= 4 only (the selected planes are all a stage loads)
+    if constexpr (ACT == mglu::kSwish && NM >= 1) {
+      if (!cl.G || cl.K <= 0 || hd->variant != 0 || B > 4) return cudaErrorNotSupported;
+      const int u = std::min(NM, B * cl.K);
+      if (u <= 1) return run_mma_nb<NM, ACT, 1, 1, true>(hd, x, B, Wt, codes, out, cl);
+      if constexpr (NM >= 2)
+        if (u <= 2) return run_mma_nb<NM, ACT, 1, 2, true>(hd, x, B, Wt, codes, out, cl);
+      if constexpr (NM >= 4)
+        if (u <= 4) return run_mma_nb<NM, ACT, 1, 4, true>(hd, x, B, Wt, codes, out, cl);
+      if constexpr (NM >= 8) return run_mma_nb<NM, ACT, 1, 8, true>(hd, x, B, Wt, codes, out, cl);
+    }
+    return cudaErrorNotSupported;
+  }
   if constexpr (ACT == mglu::kSwish && NM >= 2) {
     // (B > 4: B*K >= 5 tokens' selections cover min(n_m, 5) >= every slot count below -- all masks)
     if (cl.G && cl.K > 0 && hd->variant == 0 && B <= 4) {
@@ -991,6 +1018,31 @@ mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const 
   return forward_on_path(hd, x, B, Wt, packed, out, path, cl);
 }
 
+mglu_status mglu_forward_routed_planes(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* planes,
+                                       const float* G, int K, void* out, void* stream) {
+  mglu_status s = check_ptrs(hd, x, B, Wt, planes, out);
+  if (s != MGLU_OK) return s;
+  if (!G) return set_err(hd, MGLU_ERR_INVALID_ARG, "null gate weights");
+  if (K < 1 || K > hd->n_m) return set_err(hd, MGLU_ERR_INVALID_ARG, "K must be in [1, n_m]");
+  if (!aligned16(G)) return set_err(hd, MGLU_ERR_MISALIGNED, "gate weights must be 16-byte aligned");
+  int path, variant;
+  {
+    std::lock_guard<std::mutex> g(hd->mu);
+    path = hd->path;
+    variant = hd->variant;
+  }
+  if (!mma_can_serve(hd, B) || B > 4 || hd->act != MGLU_ACT_SWISH || variant != 0 || hd->n_m < 1 ||
+      (path != MGLU_PATH_AUTO && path != MGLU_PATH_MMA))
+    return set_err(hd, MGLU_ERR_UNSUPPORTED,
+                   "plane-major routed forward: MMA path, bf16, Swish, standard variant, 1 <= B <= 4, d % 128 == 0");
+  Call cl;
+  cl.st = (cudaStream_t)stream;
+  cl.G = G;
+  cl.K = K;
+  cl.planes = true;
+  return forward_on_path(hd, x, B, Wt, planes, out, MGLU_PATH_MMA, cl);
+}
+
 mglu_status mglu_forward_partials(mglu_handle hd, const void* x, int64_t B, const void* Wt,
                                   const void* packed, float* z, void* stream) {
   if (!hd) return MGLU_ERR_INVALID_ARG;
@@ -1217,6 +1269,29 @@ mglu_status mglu_unpack_codes_host(const uint8_t* packed, int n_m, int64_t h, in
       else codes[(e * w) >> 3] |= (uint8_t)(f << ((e * w) & 7));
     }
   return MGLU_OK;
+}
+
+mglu_status mglu_pack_planes_host(const uint8_t* packed, int n_m, int64_t h, int64_t d, uint8_t* planes) {
+  if (!packed || !planes || h < 0 || d < 0) return MGLU_ERR_INVALID_ARG;
+  if (!valid_nm(n_m) || d % 32) return MGLU_ERR_UNSUPPORTED;
+  const int64_t G = d / 32;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(packed);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(planes);
+  for (int64_t j = 0; j < h; ++j)
+    for (int64_t g = 0; g < G; ++g)
+      for (int i = 0; i < n_m; ++i) dst[((int64_t)i * h + j) * G + g] = src[(j * G + g) * n_m + i];
+  return MGLU_OK;
+}
+
+mglu_status mglu_pack_planes_device(const uint8_t* packed, int n_m, int64_t h, int64_t d, uint8_t* planes, void* stream) {
+  if (!packed || !planes || h < 0 || d < 0) return MGLU_ERR_INVALID_ARG;
+  if (!valid_nm(n_m) || d % 32) return MGLU_ERR_UNSUPPORTED;
+  if (!aligned16(packed) || !aligned16(planes)) return MGLU_ERR_MISALIGNED;
+  const int64_t n = h * (d / 32) * n_m;
+  if (n == 0) return MGLU_OK;
+  mglu::planes_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const uint32_t*>(packed), n_m, h, d / 32, reinterpret_cast<uint32_t*>(planes));
+  return device_launch_check(cudaGetLastError());
 }
 
 mglu_status mglu_pack_masks_device(const uint8_t* bits, int n_m, int64_t h, int64_t d, uint8_t* packed,

@@ -45,4 +45,15 @@ __global__ void unpack_kernel(const uint32_t* __restrict__ words, int n_m, int64
   }
 }
 
+// R3 (interleaved: word (j, g, i)) -> plane-major (word (i, j, g)): one thread per word
+__global__ void planes_kernel(const uint32_t* __restrict__ src, int n_m, int64_t h, int64_t groups,
+                              uint32_t* __restrict__ dst) {
+  const int64_t n = h * groups * n_m;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n; w += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(w % n_m);
+    const int64_t jg = w / n_m;                              // j * groups + g
+    dst[(int64_t)i * h * groups + jg] = src[w];
+  }
+}
+
 }  // namespace mglu

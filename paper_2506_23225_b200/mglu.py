@@ -69,6 +69,9 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "mglu_forward_host": ([vp, vp, i64, vp, vp, vp, vp], c_int),
         "mglu_router_topk": ([vp, vp, i64, vp, c_int, vp, vp], c_int),
         "mglu_forward_routed": ([vp, vp, i64, vp, vp, vp, c_int, vp, vp], c_int),
+        "mglu_forward_routed_planes": ([vp, vp, i64, vp, vp, vp, c_int, vp, vp], c_int),
+        "mglu_pack_planes_host": ([vp, c_int, i64, i64, vp], c_int),
+        "mglu_pack_planes_device": ([vp, c_int, i64, i64, vp, vp], c_int),
         "mglu_packed_mask_bytes": ([i64, i64, c_int], sz),
         "mglu_pack_masks_host": ([vp, c_int, i64, i64, vp], c_int),
         "mglu_code_stream_bytes": ([i64, i64, c_int], sz),
@@ -237,6 +240,26 @@ def mglu_unpack_codes_host(packed: np.ndarray, n_m: int, h: int, d: int, w: int)
     return out
 
 
+def mglu_pack_planes_host(packed: np.ndarray, n_m: int, h: int, d: int) -> np.ndarray:
+    """Interleaved packed codes -> the plane-major layout (include/mglu.h, row f2)."""
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    if packed.size != mglu_packed_mask_bytes(d, h, n_m):
+        raise MgluError(MGLU_ERR_INVALID_ARG, "packed codes size mismatch")
+    out = np.empty_like(packed)
+    _check(load_library().mglu_pack_planes_host(_ptr(packed), n_m, h, d, _ptr(out)), None, "pack_planes_host")
+    return out
+
+
+def mglu_pack_planes_device(packed: torch.Tensor, n_m: int, h: int, d: int, stream=None) -> torch.Tensor:
+    assert packed.is_cuda and packed.dtype == torch.uint8 and packed.is_contiguous()
+    if packed.numel() != mglu_packed_mask_bytes(d, h, n_m):
+        raise MgluError(MGLU_ERR_INVALID_ARG, "packed codes size mismatch")
+    out = torch.empty_like(packed)
+    _check(load_library().mglu_pack_planes_device(_ptr(packed), n_m, h, d, _ptr(out),
+                                                  _stream_ptr(stream, packed.device)), None, "pack_planes_device")
+    return out
+
+
 def mglu_pack_masks_device(bits: torch.Tensor, stream=None) -> torch.Tensor:
     assert bits.is_cuda and bits.dtype == torch.uint8 and bits.is_contiguous()
     n_m, h, d = bits.shape
@@ -383,6 +406,22 @@ class Mglu:
         else:
             self._check_out(out, B, x)
         mglu_forward_routed(self.handle, x, B, Wt, packed, G, K, out, stream)
+        return out
+
+    def forward_routed_planes(self, x: torch.Tensor, Wt: torch.Tensor, planes: torch.Tensor, G: torch.Tensor,
+                              K: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """forward_routed on plane-major codes (mglu_pack_planes_*): reads W + the selected planes."""
+        self._check_inputs(x, Wt, planes)
+        B = x.shape[0]
+        if G.dtype != torch.float32 or tuple(G.shape) != (B, self.n_m) or not G.is_contiguous():
+            raise MgluError(MGLU_ERR_INVALID_ARG, "G must be a contiguous fp32 [B][n_m] tensor")
+        if out is None:
+            out = torch.empty((B, self.h), dtype=TORCH_DTYPE[self.dtype], device=x.device)
+        else:
+            self._check_out(out, B, x)
+        _check(load_library().mglu_forward_routed_planes(self.handle, _ptr(x), B, _ptr(Wt), _ptr(planes), _ptr(G), K,
+                                                         _ptr(out), _stream_ptr(stream, x.device)),
+               self.handle, "mglu_forward_routed_planes")
         return out
 
     def forward_partials(self, x, Wt, packed, stream=None) -> torch.Tensor:
