@@ -48,9 +48,10 @@
  * caller's next synchronisation, as in CUDA.
  *
  * Threading: use a handle from ONE stream at a time (one handle per concurrently running stream).
- * The handle holds per-call state: the batched-decode workspace and tile tickets (MGLU_PATH_TCDEC,
- * which AUTO picks for bf16 and 5 <= B <= 64, and for n_m = 8 on layers with h >= 8192 from B = 1)
- * and mglu_forward_host's device staging buffers.  Calls on different handles may run
+ * The handle holds per-call state: the stream-K workspace and tile tickets (MGLU_PATH_TCDEC, which
+ * AUTO picks for bf16 and 5 <= B <= 16 on narrow layers, and for n_m = 8 on layers with h >= 8192
+ * from B = 1; the row split MGLU_PATH_TCROW keeps none) and mglu_forward_host's device staging
+ * buffers.  Calls on different handles may run
  * concurrently on any streams (the kernels never wait on another CTA, so concurrent kernels always
  * make progress).  mglu_set_path / mglu_set_variant / mglu_set_debug and the descriptor cache are
  * guarded by a mutex.
@@ -88,8 +89,9 @@ typedef enum {
 
 typedef enum { MGLU_BF16 = 0, MGLU_F32 = 1 } mglu_dtype;
 
-/* Kernel regime.  AUTO picks by dtype and B (bf16 B <= 4 MMA, 5..24 TCDEC,
- * larger TCGEN05; fp32 SIMT; a path that refuses the shape falls through).  The others force one
+/* Kernel regime.  AUTO picks by dtype and B (bf16 B <= 4 MMA, 5..48 TCROW on layers
+ * with >= 64 rows per SM (else TCDEC up to 16), larger TCGEN05; n_m = 16 TCGEN05; fp32 SIMT; a path
+ * that refuses the shape falls through).  The others force one
  * kernel (for tests and benchmarks); forcing a path that cannot serve the configuration makes
  * mglu_forward return MGLU_ERR_UNSUPPORTED. */
 typedef enum {

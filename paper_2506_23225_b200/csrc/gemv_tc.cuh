@@ -49,6 +49,9 @@
 
 namespace mglu {
 
+#ifndef MGLU_SK_ABL
+#define MGLU_SK_ABL 0   // timing ablations (wrong results): 1 no sign flips, 2 no masked-copy stores, 3 t's MMA only
+#endif
 #ifndef MGLU_SK_EPI_CH
 #define MGLU_SK_EPI_CH 4 // epilogue tokens per chunk (8 and 16 measured slower, profiles/r01_tcdec_experiments.txt §11)
 #endif
@@ -91,7 +94,10 @@ template <int NM, int BN, int MG> struct SkCfg {
   static constexpr int NOP = NM + 1;
   static constexpr int KS = 128;                          // unit width (columns)
   // A-stage width: one 32-column mask group (16 at n_m = 8 measured slower: 169 vs 129 us on config 5)
-  static constexpr int KA = 32;
+#ifndef MGLU_SK_KA
+#define MGLU_SK_KA 32
+#endif
+  static constexpr int KA = NM >= 8 ? 32 : MGLU_SK_KA;
   static constexpr int APS = KS / KA;                     // A-stages per unit
   static constexpr int SLOT = NOP * KA / 2;               // TMEM columns of an A slot (W + n_m copies)
   static constexpr int ACC = NOP * BN;                    // TMEM columns of an accumulator set
@@ -170,7 +176,10 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
   constexpr int ACC = C::ACC, CWORDS = C::CWORDS, WB = C::WB, XB = C::XB, KS = C::KS;
   constexpr int WW = KA / 2;                               // 32-bit words (bf16 pairs) of an A-stage row
   constexpr int APG = APS / MG;                            // A-stages per unit of one masker group
-  constexpr int LG = NM >= 8 ? 1 : APG;                    // A-stages a masker holds in registers at once
+#ifndef MGLU_SK_LG1
+#define MGLU_SK_LG1 1   // one A-stage in registers at a time: 1-1.5 % faster than two at B = 8..32 (profiles/r02/tc_gemv_experiments.txt)
+#endif
+  constexpr int LG = (NM >= 8 || MGLU_SK_LG1) ? 1 : APG;   // A-stages a masker holds in registers at once
   constexpr uint32_t IDESC = idesc_bf16_f32(128, BN);
   constexpr int CH = MGLU_SK_EPI_CH;                   // tokens per epilogue chunk (multiple of 4)
   static_assert(CH % 4 == 0 && BN % CH == 0, "epilogue chunk");
@@ -318,7 +327,7 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
               const uint32_t accum = (u == lo && k16 == 0) ? 0u : 1u;
               const uint32_t asl = tmem + A_COL0 + (uint32_t)(sa * SLOT + kk * 8);
 #pragma unroll
-              for (int o = 0; o < NOP; ++o)
+              for (int o = 0; o < (MGLU_SK_ABL == 3 ? 1 : NOP); ++o)
                 tc_mma_ts(dacc + (uint32_t)(o * BN), asl + (uint32_t)(o * WW), bdesc, IDESC, accum);
             }
             tc_commit(&a_empty[sa]);
@@ -374,7 +383,7 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
             const uint32_t a0 = a_lane + (uint32_t)(sa * SLOT);
             tmem_st_n<WW>(a0, w[j]);
 #pragma unroll
-            for (int i = 0; i < NM; ++i) {
+            for (int i = 0; i < (MGLU_SK_ABL == 2 ? 0 : NM); ++i) {
               uint32_t op[WW];
               // pair q of the A-stage is pair q0 + q of its 32-column group: bits (q0 + q, q0 + q + 16)
               // of the group's word; shifting the word right by q0 keeps the bits that reach the bf16
@@ -382,7 +391,7 @@ gemv_tc_kernel(const SkParams p, const __grid_constant__ CUtensorMap mW, const _
               const uint32_t word = cw[j][i] >> (((g + (j0 + j) * MG) * KA & 31) >> 1);
 #pragma unroll
               for (int q = 0; q < WW; ++q)
-                op[q] = sign_flip(w[j][q], word, 1u << (15 - q));
+                op[q] = MGLU_SK_ABL == 1 ? (w[j][q] ^ word) : sign_flip(w[j][q], word, 1u << (15 - q));
               tmem_st_n<WW>(a0 + (uint32_t)((1 + i) * WW), op);
             }
             tmem_st_wait();

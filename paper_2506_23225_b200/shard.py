@@ -85,9 +85,11 @@ def ffn_forward_tp(up, down, x: torch.Tensor, Wt_g: torch.Tensor, packed_g: torc
                    Wo_g: torch.Tensor, group=None) -> torch.Tensor:
     """One rank's SwiMGLU FFN block under tensor parallelism: the column-sharded up-projection
     y_g = MGLU_g(x) [B][h_g] (no exchange), the row-sharded down-projection partial y_g Wo_g^T
-    [B][d] (an n_m = 0 dense handle), then ONE all-reduce (sum, fp32) of the partials over the
-    group -- the step's only collective (NCCL over NVLink on GPUs, gloo on CPU).  `up` / `down`
-    are Mglu handles of shapes (d, h_g, n_m) and (h_g, d, 0)."""
+    [B][d] (an n_m = 0 dense handle; each rank's partial is rounded to bf16 by that handle's
+    output, then widened), then ONE all-reduce (sum, in fp32) of the partials over the group -- the
+    step's only collective (NCCL over NVLink on GPUs, gloo on CPU).  `up` / `down` are Mglu handles
+    of shapes (d, h_g, n_m) and (h_g, d, 0); the dense handle needs h_g % 128 == 0 (shard_bounds
+    gives that for h % (128 G) == 0, e.g. the Llama shapes at G in {1, 2, 4, 8})."""
     import torch.distributed as dist
     y_g = up.forward(x, Wt_g, packed_g)
     part = down.forward(y_g, Wo_g, None).float()
