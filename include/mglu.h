@@ -162,6 +162,19 @@ mglu_status mglu_router_topk(mglu_handle hd, const void* x, int64_t B, const voi
 mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* packed,
                                 const float* G, int K, void* out, void* stream);
 
+/* Row f1, fused: the SwiMGLU FFN block out = MGLU(x) Wo^T (DESIGN R19) in ONE launch.
+ *   up    an MGLU handle (d, h, n_m in {1, 2, 4, 8}, any act), down a DENSE handle (h, d_out, 0);
+ *   x [B][d], Wt [h][d], packed (interleaved codes), Wo [d_out][h] (nn.Linear(h, d_out).weight),
+ *   y_mid [B][h] bf16 (written: MGLU(x), rounded to bf16 -- the value the down-projection reads),
+ *   out [B][d_out] bf16.  Every pointer device, 16-byte aligned, borrowed.
+ * The grid streams the up-projection's W and codes and then W_o through one shared-memory ring,
+ * with a grid-wide barrier (cooperative launch: all CTAs resident, one per SM) between the phases;
+ * the result equals up.forward followed by down.forward bit for bit.  bf16, 1 <= B <= 4,
+ * d % 128 == 0 and h % 128 == 0, Swish at n_m = 8, else UNSUPPORTED; mismatched handles INVALID_ARG.  The up
+ * handle keeps the barrier state (8 bytes, allocated on the first call). */
+mglu_status mglu_ffn_forward(mglu_handle up, mglu_handle down, const void* x, int64_t B, const void* Wt,
+                             const void* packed, const void* Wo, void* y_mid, void* out, void* stream);
+
 /* Top-K routed forward on PLANE-MAJOR codes (mglu_pack_planes_*): the same result as
  * mglu_forward_routed on the interleaved codes (bit-identical: same kernel arithmetic), but each
  * stage streams W and only the planes some token selected.  MMA path only: bf16, Swish, standard

@@ -39,7 +39,7 @@ def needs_build() -> bool:
 
 # kernels on the timed hot path: the build fails if any instantiation of these uses a stack frame
 # or local memory (register spills -- the failure mode of P:445-447 at n_m = 8)
-HOT_KERNELS = ("gemv_mma_kernel", "gemv_tc_kernel", "gemm_tc_kernel", "router_topk_kernel")
+HOT_KERNELS = ("gemv_mma_kernel", "gemv_tc_kernel", "gemm_tc_kernel", "router_topk_kernel", "ffn_mma_kernel")
 
 
 def resource_usage(lib: str) -> dict:

@@ -135,129 +135,120 @@ __device__ __forceinline__ void dec_stage_of(int i, int nfull, int rem, int d, i
 // batch selected, so a routed call reads W plus K (not n_m) bits per element (row f2).
 // maps.c[ti] then views the planes as one [n_m h][d/32] word tensor with boxes of 8T rows x KS/32
 // words; the selection needs G, so this producer starts after griddepcontrol.wait.
-template <int NM, int ACT, int NB, int KSEL, bool PL = false>
-__global__ void __launch_bounds__(kDecThreads, 1)
-gemv_mma_kernel(const DecParams p, const __grid_constant__ DecMaps maps) {
+// a CTA's share of a layer: whole 8-row tiles [tile0, tile0 + ntiles) processed in rounds
+struct DecGeo {
+  int r0, nrows, nfull, rem, nstages, d;
+};
+__device__ __forceinline__ DecGeo dec_geo(const DecParams& p, int cta) {
+  DecGeo g;
+  const int tile0 = cta * p.tiles_base + min(cta, p.tiles_rem);
+  const int ntiles = p.tiles_base + (cta < p.tiles_rem ? 1 : 0);
+  g.r0 = 8 * tile0;
+  g.nrows = min(8 * ntiles, p.h - g.r0);
+  g.d = p.d;
+  g.nfull = ntiles >> 3;
+  g.rem = ntiles & 7;
+  g.nstages = g.nfull * dec_round_stages(0, g.d);
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+    if ((g.rem >> b) & 1) g.nstages += dec_round_stages(3 - b, g.d);
+  return g;
+}
+
+// one thread: the TMA producer of the CTA's stages (ring position s / ph carried across calls:
+// the fused FFN kernel streams its two phases through one ring)
+template <int NM, int ACT, int NB, int KSEL, bool PL, int SB>
+__device__ __forceinline__ void dec_produce(const DecParams& p, const DecMaps& maps, uint8_t* ring, uint64_t* full,
+                                            uint64_t* empty, int S, const DecGeo& geo, int& s, uint32_t& ph) {
   static_assert(!PL || KSEL > 0, "plane-major codes: routed calls only");
   constexpr int SPAN = dec_code_span<NM>();
-  constexpr int SB = dec_stage_bytes_pl<NM, KSEL, PL>();
   constexpr int NACC = NB * ((KSEL > 0 ? KSEL : NM) + 1);
+  (void)SPAN; (void)NACC;
+  const int r0 = geo.r0, nrows = geo.nrows, nfull = geo.nfull, rem = geo.rem, nstages = geo.nstages, d = geo.d;
+  (void)nrows; (void)nstages;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      prefetch_tmap(&maps.w[t]);
+      if (NM > 0) prefetch_tmap(&maps.c[t]);
+    }
+    const uint64_t pol = policy_evict_first();
+    int psel[PL ? KSEL : 1];
+    int pn = 0;
+    if constexpr (PL) {
+      // the ring's first stages of W (constant weights) stream before the PDL wait: their
+      // barriers expect the W bytes now, the selected planes' bytes and the arrival after it
+      const int pre = min(S, nstages);
+      for (int i = 0; i < pre; ++i) {
+        int ti, row0, ks;
+        dec_stage_of(i, nfull, rem, d, ti, row0, ks);
+        mbar_expect_tx(&full[i], (uint32_t)(16384 * 2));
+        tma_load_3d_hint(ring + (size_t)i * SB, &maps.w[ti], 0, r0 + row0, ks * (256 << ti) / 64, &full[i], pol);
+      }
+      pdl_wait();                                          // G comes from the router launch
+      pn = dec_select<NM, KSEL>(p.G, p.B, psel);
+      for (int i = 0; i < pre; ++i) {
+        int ti, row0, ks;
+        dec_stage_of(i, nfull, rem, d, ti, row0, ks);
+        mbar_arrive_expect_tx(&full[i], (uint32_t)(pn * kDecPlaneBytes));
+#pragma unroll
+        for (int k = 0; k < KSEL; ++k)
+          if (k < pn) tma_load_2d_hint(ring + (size_t)i * SB + kDecWBytes + k * kDecPlaneBytes, &maps.c[ti],
+                                       ks * (256 << ti) / 32, psel[k] * p.h + r0 + row0, &full[i], pol);
+      }
+    }
+    for (int i = 0; i < nstages; ++i) {
+      int ti, row0, ks;
+      dec_stage_of(i, nfull, rem, d, ti, row0, ks);
+      const int k0 = ks * (256 << ti);
+      if constexpr (PL) {
+        if (i < S) { if (++s == S) { s = 0; ph ^= 1; } continue; }   // issued above
+      }
+      mbar_wait(&empty[s], ph ^ 1);
+      uint8_t* wst = ring + (size_t)s * SB;
+      if constexpr (PL) {
+        // W + the selected planes' words of the stage's rows (8T rows x KS/32 words each)
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(16384 * 2 + pn * kDecPlaneBytes));
+        tma_load_3d_hint(wst, &maps.w[ti], 0, r0 + row0, k0 / 64, &full[s], pol);
+#pragma unroll
+        for (int k = 0; k < KSEL; ++k)
+          if (k < pn) tma_load_2d_hint(wst + kDecWBytes + k * kDecPlaneBytes, &maps.c[ti], k0 / 32,
+                                       psel[k] * p.h + r0 + row0, &full[s], pol);
+        if (++s == S) { s = 0; ph ^= 1; }
+        continue;
+      }
+      mbar_arrive_expect_tx(&full[s], (uint32_t)(16384 * 2 + 16384 / 128 * SPAN));
+      tma_load_3d_hint(wst, &maps.w[ti], 0, r0 + row0, k0 / 64, &full[s], pol);
+      if constexpr (NM > 0) tma_load_3d_hint(wst + kDecWBytes, &maps.c[ti], 0, r0 + row0, k0 / 128, &full[s], pol);
+      if (i == S - 1) {
+        // ring filled: the next l2pf stages go to L2 once, so HBM keeps streaming while the
+        // consumers wait for the previous grid (PDL) and for x
+        for (int f = S; f < min(nstages, S + p.l2pf); ++f) {
+          int fti, frow, fks;
+          dec_stage_of(f, nfull, rem, d, fti, frow, fks);
+          const int fk0 = fks * (256 << fti);
+          tma_prefetch_3d(&maps.w[fti], 0, r0 + frow, fk0 / 64);
+          if constexpr (NM > 0) tma_prefetch_3d(&maps.c[fti], 0, r0 + frow, fk0 / 128);
+        }
+      }
+      if (++s == S) { s = 0; ph ^= 1; }
+    }
+}
+
+// the 16 consumer warps: x staging, the rounds of MMAs over the stages, the epilogue
+template <int NM, int ACT, int NB, int KSEL, bool PL, int SB>
+__device__ __forceinline__ void dec_consume(const DecParams& p, uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                            float* part, uint32_t* xs, int S, const DecGeo& geo, int& s, uint32_t& ph) {
+  static_assert(!PL || KSEL > 0, "plane-major codes: routed calls only");
+  constexpr int SPAN = dec_code_span<NM>();
+  constexpr int NACC = NB * ((KSEL > 0 ? KSEL : NM) + 1);
+  (void)SPAN; (void)NACC;
   // 32-column steps loaded per register group: all 4 of a stage, or 2 / 1 where the staged
   // operands would not fit beside the accumulators (n_m = 8; two token groups with n_m >= 4).
   // (17 warps per CTA leave 96 registers per thread: one SM sub-partition holds 5 of them.)
   constexpr int kGrp = (NB == 2 && (KSEL > 0 ? KSEL : NM) >= 4) ? 1 : ((KSEL > 0 ? KSEL : NM) * NB > 4) ? 2 : 4;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  // ring depth: the CTAs owning one tile more than the others keep one stage more in flight, so
-  // their share of the HBM bandwidth grows with their work and they do not finish last (the next
-  // call's consumers wait for this grid's last CTA)
-  const int S = (p.tiles_rem && (int)blockIdx.x >= p.tiles_rem) ? p.stages - p.light_drop : p.stages;
-  uint8_t* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB);
-  uint64_t* empty = full + S;
-  float* part = reinterpret_cast<float*>(empty + S);     // [16 warps][32 lanes][NACC]
-  uint32_t* xs = reinterpret_cast<uint32_t*>(part + kDecConsumers * 32 * NACC);
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cta = blockIdx.x;
-  const int tile0 = cta * p.tiles_base + min(cta, p.tiles_rem);
-  const int ntiles = p.tiles_base + (cta < p.tiles_rem ? 1 : 0);
-  const int r0 = 8 * tile0;
-  const int nrows = min(8 * ntiles, p.h - r0);
-  const int d = p.d;
-  const int nfull = ntiles >> 3, rem = ntiles & 7;
-  int nstages = nfull * dec_round_stages(0, d);
-#pragma unroll
-  for (int b = 0; b < 3; ++b)
-    if ((rem >> b) & 1) nstages += dec_round_stages(3 - b, d);
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kDecConsumers);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  pdl_launch_dependents();
-
-  if (warp == kDecConsumers) {
-    // ------------------------------------------------------------ producer (one thread)
-    // two TMA ops per stage (W box + code box), no over-read: the boxes of a round hold exactly its
-    // 8T rows (a ragged last tile of the layer is zero-filled past h).
-    if (lane == 0) {
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        prefetch_tmap(&maps.w[t]);
-        if (NM > 0) prefetch_tmap(&maps.c[t]);
-      }
-      const uint64_t pol = policy_evict_first();
-      int psel[PL ? KSEL : 1];
-      int pn = 0;
-      if constexpr (PL) {
-        // the ring's first stages of W (constant weights) stream before the PDL wait: their
-        // barriers expect the W bytes now, the selected planes' bytes and the arrival after it
-        const int pre = min(S, nstages);
-        for (int i = 0; i < pre; ++i) {
-          int ti, row0, ks;
-          dec_stage_of(i, nfull, rem, d, ti, row0, ks);
-          mbar_expect_tx(&full[i], (uint32_t)(16384 * 2));
-          tma_load_3d_hint(ring + (size_t)i * SB, &maps.w[ti], 0, r0 + row0, ks * (256 << ti) / 64, &full[i], pol);
-        }
-        pdl_wait();                                          // G comes from the router launch
-        pn = dec_select<NM, KSEL>(p.G, p.B, psel);
-        for (int i = 0; i < pre; ++i) {
-          int ti, row0, ks;
-          dec_stage_of(i, nfull, rem, d, ti, row0, ks);
-          mbar_arrive_expect_tx(&full[i], (uint32_t)(pn * kDecPlaneBytes));
-#pragma unroll
-          for (int k = 0; k < KSEL; ++k)
-            if (k < pn) tma_load_2d_hint(ring + (size_t)i * SB + kDecWBytes + k * kDecPlaneBytes, &maps.c[ti],
-                                         ks * (256 << ti) / 32, psel[k] * p.h + r0 + row0, &full[i], pol);
-        }
-      }
-      int s = 0;
-      uint32_t ph = 0;
-      for (int i = 0; i < nstages; ++i) {
-        int ti, row0, ks;
-        dec_stage_of(i, nfull, rem, d, ti, row0, ks);
-        const int k0 = ks * (256 << ti);
-        if constexpr (PL) {
-          if (i < S) { if (++s == S) { s = 0; ph ^= 1; } continue; }   // issued above
-        }
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* wst = ring + (size_t)s * SB;
-        if constexpr (PL) {
-          // W + the selected planes' words of the stage's rows (8T rows x KS/32 words each)
-          mbar_arrive_expect_tx(&full[s], (uint32_t)(16384 * 2 + pn * kDecPlaneBytes));
-          tma_load_3d_hint(wst, &maps.w[ti], 0, r0 + row0, k0 / 64, &full[s], pol);
-#pragma unroll
-          for (int k = 0; k < KSEL; ++k)
-            if (k < pn) tma_load_2d_hint(wst + kDecWBytes + k * kDecPlaneBytes, &maps.c[ti], k0 / 32,
-                                         psel[k] * p.h + r0 + row0, &full[s], pol);
-          if (++s == S) { s = 0; ph ^= 1; }
-          continue;
-        }
-        mbar_arrive_expect_tx(&full[s], (uint32_t)(16384 * 2 + 16384 / 128 * SPAN));
-        tma_load_3d_hint(wst, &maps.w[ti], 0, r0 + row0, k0 / 64, &full[s], pol);
-        if constexpr (NM > 0) tma_load_3d_hint(wst + kDecWBytes, &maps.c[ti], 0, r0 + row0, k0 / 128, &full[s], pol);
-        if (i == S - 1) {
-          // ring filled: the next l2pf stages go to L2 once, so HBM keeps streaming while the
-          // consumers wait for the previous grid (PDL) and for x
-          for (int f = S; f < min(nstages, S + p.l2pf); ++f) {
-            int fti, frow, fks;
-            dec_stage_of(f, nfull, rem, d, fti, frow, fks);
-            const int fk0 = fks * (256 << fti);
-            tma_prefetch_3d(&maps.w[fti], 0, r0 + frow, fk0 / 64);
-            if constexpr (NM > 0) tma_prefetch_3d(&maps.c[fti], 0, r0 + frow, fk0 / 128);
-          }
-        }
-        if (++s == S) { s = 0; ph ^= 1; }
-      }
-    }
-    return;
-  }
-
-  // -------------------------------------------------------------- consumers
+  const int r0 = geo.r0, nrows = geo.nrows, nfull = geo.nfull, rem = geo.rem, nstages = geo.nstages, d = geo.d;
+  (void)nrows; (void)nstages;
   const int g = lane >> 2, c = lane & 3;
   const int B = p.B;
   const int prow = (g >> 1) + 4 * (g & 1);                 // pi(g): tile-local real row
@@ -332,8 +323,6 @@ gemv_mma_kernel(const DecParams p, const __grid_constant__ DecMaps maps) {
 #pragma unroll
       for (int v = 0; v < 4; ++v) acc[nb][a][v] = 0.f;
 
-  int s = 0;
-  uint32_t ph = 0;
   int row0 = 0;
   const int nrounds = nfull + __popc(rem);
   for (int rho = 0; rho < nrounds; ++rho) {
@@ -519,6 +508,117 @@ gemv_mma_kernel(const DecParams p, const __grid_constant__ DecMaps maps) {
     named_bar_sync(1, kDecConsumers * 32);                  // partials are rewritten next round
     row0 += rows;
   }
+}
+
+template <int NM, int ACT, int NB, int KSEL, bool PL = false>
+__global__ void __launch_bounds__(kDecThreads, 1)
+gemv_mma_kernel(const DecParams p, const __grid_constant__ DecMaps maps) {
+  constexpr int SB = dec_stage_bytes_pl<NM, KSEL, PL>();
+  constexpr int NACC = NB * ((KSEL > 0 ? KSEL : NM) + 1);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  // ring depth: the CTAs owning one tile more than the others keep one stage more in flight, so
+  // their share of the HBM bandwidth grows with their work and they do not finish last (the next
+  // call's consumers wait for this grid's last CTA)
+  const int S = (p.tiles_rem && (int)blockIdx.x >= p.tiles_rem) ? p.stages - p.light_drop : p.stages;
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB);
+  uint64_t* empty = full + S;
+  float* part = reinterpret_cast<float*>(empty + S);     // [16 warps][32 lanes][NACC]
+  uint32_t* xs = reinterpret_cast<uint32_t*>(part + kDecConsumers * 32 * NACC);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kDecConsumers);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+
+  const DecGeo geo = dec_geo(p, blockIdx.x);
+  if (warp == kDecConsumers) {
+    int s = 0;
+    uint32_t ph = 0;
+    if (lane == 0) dec_produce<NM, ACT, NB, KSEL, PL, SB>(p, maps, ring, full, empty, S, geo, s, ph);
+    return;
+  }
+  int s = 0;
+  uint32_t ph = 0;
+  dec_consume<NM, ACT, NB, KSEL, PL, SB>(p, ring, full, empty, part, xs, S, geo, s, ph);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Row f1, fused: the SwiMGLU FFN block FFN(x) = MGLU(x) W_o^T (reading R19) in ONE launch.
+// Phase 1 is the decode kernel above over the up-projection's rows (y = MGLU(x), bf16, to `p1.out`);
+// phase 2 the same kernel's dense form (n_m = 0) over W_o's rows with x = y.  Both phases stream
+// through ONE ring: the producer issues W_o's stages right after the up-projection's, so while the
+// consumers wait at the grid barrier (every CTA's y slice written) the ring fills with W_o and the
+// HBM stream never stops at the layer boundary -- the part a two-launch composition loses (the
+// dependent grid cannot start streaming until the first grid's CTAs leave the SMs).  y makes one
+// round trip through L2 (B h bf16 values); the grid barrier needs all CTAs resident (cooperative
+// launch, one CTA per SM) and resets itself (sense reversal), so repeats and graph replays work.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// one thread per CTA; bar[0] = arrivals, bar[1] = generation (both 0 at allocation)
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nctas) {
+  const unsigned gen = ld_acquire_gpu(bar + 1);
+  __threadfence();
+  if (atomicAdd(bar, 1u) == nctas - 1u) {
+    atomicExch(bar, 0u);
+    __threadfence();
+    atomicAdd(bar + 1, 1u);                                 // release the waiters
+  } else {
+    while (ld_acquire_gpu(bar + 1) == gen) __nanosleep(64);
+  }
+  __threadfence();
+}
+
+template <int NM, int ACT>
+__global__ void __launch_bounds__(kDecThreads, 1)
+ffn_mma_kernel(const DecParams p1, const __grid_constant__ DecMaps m1, const DecParams p2,
+               const __grid_constant__ DecMaps m2, unsigned* gbar) {
+  constexpr int SB = dec_stage_bytes<NM>();                 // W_o stages use the same slots
+  constexpr int NACC = NM + 1;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int S = p1.stages;
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB);
+  uint64_t* empty = full + S;
+  float* part = reinterpret_cast<float*>(empty + S);
+  uint32_t* xs = reinterpret_cast<uint32_t*>(part + kDecConsumers * 32 * NACC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kDecConsumers);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  const DecGeo g1 = dec_geo(p1, blockIdx.x), g2 = dec_geo(p2, blockIdx.x);
+  if (warp == kDecConsumers) {
+    int s = 0;
+    uint32_t ph = 0;
+    if (lane == 0) {
+      dec_produce<NM, ACT, 1, 0, false, SB>(p1, m1, ring, full, empty, S, g1, s, ph);
+      dec_produce<0, kIdentity, 1, 0, false, SB>(p2, m2, ring, full, empty, S, g2, s, ph);
+    }
+    return;
+  }
+  int s = 0;
+  uint32_t ph = 0;
+  dec_consume<NM, ACT, 1, 0, false, SB>(p1, ring, full, empty, part, xs, S, g1, s, ph);
+  __threadfence();                                          // this CTA's y slice -> visible
+  named_bar_sync(1, kDecConsumers * 32);
+  if (threadIdx.x == 0) grid_barrier(gbar, gridDim.x);
+  named_bar_sync(1, kDecConsumers * 32);
+  dec_consume<0, kIdentity, 1, 0, false, SB>(p2, ring, full, empty, part, xs, S, g2, s, ph);
 }
 
 }  // namespace mglu

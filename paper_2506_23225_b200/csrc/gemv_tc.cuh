@@ -97,7 +97,10 @@ template <int NM, int BN, int MG> struct SkCfg {
 #ifndef MGLU_SK_KA
 #define MGLU_SK_KA 32
 #endif
-  static constexpr int KA = NM >= 8 ? 32 : MGLU_SK_KA;
+#ifndef MGLU_SK_KA8
+#define MGLU_SK_KA8 32
+#endif
+  static constexpr int KA = NM >= 8 ? MGLU_SK_KA8 : MGLU_SK_KA;
   static constexpr int APS = KS / KA;                     // A-stages per unit
   static constexpr int SLOT = NOP * KA / 2;               // TMEM columns of an A slot (W + n_m copies)
   static constexpr int ACC = NOP * BN;                    // TMEM columns of an accumulator set

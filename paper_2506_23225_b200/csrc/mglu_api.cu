@@ -62,6 +62,8 @@ struct mglu_ctx {
   // training path (mglu_backward): forward streams z [B][2 n_m][h] + coefficients E [B][n_m+1][h]
   float* bw_ws = nullptr;
   size_t bw_ws_bytes = 0;
+  // fused FFN block (row f1): grid-barrier counter + generation, zeroed once, self-resetting
+  unsigned* ffn_bar = nullptr;
 
 };
 
@@ -286,6 +288,21 @@ int dec_l2pf() {
   return v;
 }
 
+// x in smem, split by pair parity and zero-padded to the last column any stage can touch (the
+// widest round type a CTA of this grid runs): u32 words per parity array
+int dec_xpar(const mglu_ctx* hd, const mglu::DecParams& p) {
+  int64_t maxcol = hd->d;
+  for (int64_t nt : {(int64_t)p.tiles_base, (int64_t)p.tiles_base + (p.tiles_rem ? 1 : 0)}) {
+    for (int ti = 0; ti < 4; ++ti) {
+      const bool used = ti == 0 ? nt >= 8 : ((nt & 7) >> (3 - ti)) & 1;
+      if (!used) continue;
+      const int64_t ks = 256 << ti;
+      maxcol = std::max<int64_t>(maxcol, (hd->d + ks - 1) / ks * ks);
+    }
+  }
+  return (int)(maxcol / 2) / 2 + 8;
+}
+
 template <int NM, int ACT, int NB, int KSEL, bool PL = false>
 cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const void* codes,
                        void* out, const Call& cl) {
@@ -308,19 +325,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   p.light_drop = 0;
   mglu::DecMaps maps;
   if (!dec_maps(hd, Wt, codes, &maps, PL)) return cudaErrorInvalidValue;
-  // x in smem, split by pair parity and zero-padded to the last column any stage can touch (the
-  // widest round type a CTA of this grid runs)
-  int64_t maxcol = hd->d;
-  for (int64_t nt : {(int64_t)p.tiles_base, (int64_t)p.tiles_base + (p.tiles_rem ? 1 : 0)}) {
-    for (int ti = 0; ti < 4; ++ti) {
-      const bool used = ti == 0 ? nt >= 8 : ((nt & 7) >> (3 - ti)) & 1;
-      if (!used) continue;
-      const int64_t ks = 256 << ti;
-      maxcol = std::max<int64_t>(maxcol, (hd->d + ks - 1) / ks * ks);
-    }
-  }
-  const int npair = (int)(maxcol / 2);
-  p.xpar = npair / 2 + 8;
+  p.xpar = dec_xpar(hd, p);
   constexpr size_t SB = mglu::dec_stage_bytes_pl<NM, KSEL, PL>();
   const size_t xbytes = (size_t)2 * B * p.xpar * 4;
   const size_t partbytes = (size_t)mglu::kDecConsumers * 32 * NB * ((KSEL > 0 ? KSEL : NM) + 1) * 4;
@@ -410,6 +415,89 @@ cudaError_t mma_nm(mglu_ctx* hd, const void* x, int B, const void* Wt, const voi
     case 2: return mma_act<2>(hd, x, B, Wt, codes, out, cl);
     case 4: return mma_act<4>(hd, x, B, Wt, codes, out, cl);
     default: return mma_act<8>(hd, x, B, Wt, codes, out, cl);
+  }
+}
+
+// ------------------------------------------------------------------ fused FFN block (row f1)
+// DecParams of one handle's decode pass over `ncta` CTAs (whole 8-row tiles per CTA)
+mglu::DecParams dec_params(const mglu_ctx* hd, const void* x, int B, void* out, int64_t ncta) {
+  mglu::DecParams p;
+  p.x = (const __nv_bfloat16*)x;
+  p.out = (__nv_bfloat16*)out;
+  p.G = nullptr;
+  p.z = nullptr;
+  p.variant = hd->variant;
+  p.act = hd->act;
+  p.B = B;
+  p.d = (int)hd->d;
+  p.h = (int)hd->h;
+  const int64_t tiles = (hd->h + 7) / 8;
+  p.tiles_base = (int)(tiles / ncta);
+  p.tiles_rem = (int)(tiles % ncta);
+  p.l2pf = 0;
+  p.light_drop = 0;
+  p.xpar = dec_xpar(hd, p);
+  return p;
+}
+
+template <int NM, int ACT>
+cudaError_t run_ffn(mglu_ctx* up, mglu_ctx* down, const void* x, int B, const void* Wt, const void* codes,
+                    const void* Wo, void* ymid, void* out, cudaStream_t st) {
+  const int64_t ncta = std::min<int64_t>((up->h + 7) / 8, up->num_sms);
+  mglu::DecParams p1 = dec_params(up, x, B, ymid, ncta);
+  mglu::DecParams p2 = dec_params(down, ymid, B, out, ncta);
+  mglu::DecMaps m1, m2;
+  if (!dec_maps(up, Wt, codes, &m1) || !dec_maps(down, Wo, nullptr, &m2)) return cudaErrorInvalidValue;
+  constexpr size_t SB = mglu::dec_stage_bytes<NM>();
+  const size_t xbytes = (size_t)2 * B * std::max(p1.xpar, p2.xpar) * 4;
+  const size_t partbytes = (size_t)mglu::kDecConsumers * 32 * (NM + 1) * 4;
+  const size_t fixed = xbytes + partbytes + 1024;
+  const size_t cap = std::min<size_t>((size_t)up->max_smem_optin, (size_t)dec_smem_kb() * 1024 + 32 * 1024);
+  if (cap < fixed + 2 * (SB + 16)) return cudaErrorInvalidConfiguration;
+  const int S = (int)std::min<size_t>(8, (cap - fixed) / (SB + 16));
+  p1.stages = p2.stages = S;
+  const size_t smem = (size_t)S * SB + 2 * S * sizeof(uint64_t) + partbytes + xbytes;
+  auto kern = mglu::ffn_mma_kernel<NM, ACT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (!up->ffn_bar) {
+    if ((e = cudaMalloc(&up->ffn_bar, 2 * sizeof(unsigned))) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(up->ffn_bar, 0, 2 * sizeof(unsigned), st)) != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ncta);
+  cfg.blockDim = dim3(mglu::kDecThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;               // the grid barrier needs every CTA resident
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // W streams before the previous call ends
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  e = cudaLaunchKernelEx(&cfg, kern, p1, m1, p2, m2, up->ffn_bar);
+  if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {   // runtime without cooperative + PDL
+    (void)cudaGetLastError();
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, p1, m1, p2, m2, up->ffn_bar);
+  }
+  return e;
+}
+
+cudaError_t ffn_nm(mglu_ctx* up, mglu_ctx* down, const void* x, int B, const void* Wt, const void* codes,
+                   const void* Wo, void* ymid, void* out, cudaStream_t st) {
+  const bool sw = up->act == MGLU_ACT_SWISH;
+  switch (up->n_m) {
+    case 1: return sw ? run_ffn<1, mglu::kSwish>(up, down, x, B, Wt, codes, Wo, ymid, out, st)
+                      : run_ffn<1, mglu::kRuntimeAct>(up, down, x, B, Wt, codes, Wo, ymid, out, st);
+    case 2: return sw ? run_ffn<2, mglu::kSwish>(up, down, x, B, Wt, codes, Wo, ymid, out, st)
+                      : run_ffn<2, mglu::kRuntimeAct>(up, down, x, B, Wt, codes, Wo, ymid, out, st);
+    case 4: return sw ? run_ffn<4, mglu::kSwish>(up, down, x, B, Wt, codes, Wo, ymid, out, st)
+                      : run_ffn<4, mglu::kRuntimeAct>(up, down, x, B, Wt, codes, Wo, ymid, out, st);
+    case 8: return sw ? run_ffn<8, mglu::kSwish>(up, down, x, B, Wt, codes, Wo, ymid, out, st)
+                      : cudaErrorNotSupported;     // (the runtime-g n_m = 8 fused kernel would spill)
+    default: return cudaErrorInvalidValue;
   }
 }
 
@@ -692,6 +780,10 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
 template <int NM, int BN>
 cudaError_t run_sk_mg(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
                       const Call& cl) {
+#ifndef MGLU_SK_MG8
+#define MGLU_SK_MG8 2
+#endif
+  if constexpr (NM >= 8 && MGLU_SK_MG8 == 4 && mglu::SkCfg<NM, BN, 4>::ok) return run_sk_bn<NM, BN, 4>(hd, x, B, Wt, codes, out, cl);
   if constexpr (mglu::SkCfg<NM, BN, 2>::ok) return run_sk_bn<NM, BN, 2>(hd, x, B, Wt, codes, out, cl);
   else return run_sk_bn<NM, BN, 1>(hd, x, B, Wt, codes, out, cl);
 }
@@ -829,6 +921,7 @@ mglu_status mglu_destroy(mglu_handle hd) {
   if (hd->sk_ws) cudaFree(hd->sk_ws);
   if (hd->sk_tickets) cudaFree(hd->sk_tickets);
   if (hd->bw_ws) cudaFree(hd->bw_ws);
+  if (hd->ffn_bar) cudaFree(hd->ffn_bar);
   cudaSetDevice(prev);
   delete hd;
   return MGLU_OK;
@@ -1016,6 +1109,31 @@ mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const 
   cl.G = G;
   cl.K = K;
   return forward_on_path(hd, x, B, Wt, packed, out, path, cl);
+}
+
+mglu_status mglu_ffn_forward(mglu_handle up, mglu_handle down, const void* x, int64_t B, const void* Wt,
+                             const void* packed, const void* Wo, void* y_mid, void* out, void* stream) {
+  if (!up || !down) return MGLU_ERR_INVALID_ARG;
+  mglu_status s = check_ptrs(up, x, B, Wt, packed, y_mid);
+  if (s != MGLU_OK) return s;
+  if (!Wo || !out) return set_err(up, MGLU_ERR_INVALID_ARG, "null W_o / out");
+  if (!aligned16(Wo) || !aligned16(out)) return set_err(up, MGLU_ERR_MISALIGNED, "W_o / out must be 16-byte aligned");
+  if (down->n_m != 0 || down->d != up->h || down->device != up->device || down->dtype != MGLU_BF16)
+    return set_err(up, MGLU_ERR_INVALID_ARG, "down must be a dense (n_m = 0) bf16 handle with d = up.h on up's device");
+  if (B == 0) return MGLU_OK;
+  if (!fast_nm(up->n_m) || B > 4 || !mma_can_serve(up, B) || !mma_can_serve(down, B) ||
+      (up->n_m == 8 && up->act != MGLU_ACT_SWISH))
+    return set_err(up, MGLU_ERR_UNSUPPORTED,
+                   "fused FFN: bf16, n_m in {1, 2, 4, 8} (Swish at n_m = 8), 1 <= B <= 4, d % 128 == 0 and h % 128 == 0");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != up->device) cudaSetDevice(up->device);
+  const cudaError_t e = ffn_nm(up, down, x, (int)B, Wt, packed, Wo, y_mid, out, (cudaStream_t)stream);
+  if (prev != up->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(up, e, "mglu_ffn_forward launch");
+  up->last_path = MGLU_PATH_MMA;
+  up->last_launches = 1;
+  return MGLU_OK;
 }
 
 mglu_status mglu_forward_routed_planes(mglu_handle hd, const void* x, int64_t B, const void* Wt, const void* planes,

@@ -70,6 +70,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "mglu_router_topk": ([vp, vp, i64, vp, c_int, vp, vp], c_int),
         "mglu_forward_routed": ([vp, vp, i64, vp, vp, vp, c_int, vp, vp], c_int),
         "mglu_forward_routed_planes": ([vp, vp, i64, vp, vp, vp, c_int, vp, vp], c_int),
+        "mglu_ffn_forward": ([vp, vp, vp, i64, vp, vp, vp, vp, vp, vp], c_int),
         "mglu_pack_planes_host": ([vp, c_int, i64, i64, vp], c_int),
         "mglu_pack_planes_device": ([vp, c_int, i64, i64, vp, vp], c_int),
         "mglu_packed_mask_bytes": ([i64, i64, c_int], sz),
@@ -237,6 +238,28 @@ def mglu_unpack_codes_host(packed: np.ndarray, n_m: int, h: int, d: int, w: int)
     packed = np.ascontiguousarray(packed, dtype=np.uint8)
     out = np.empty(mglu_code_stream_bytes(d, h, w), dtype=np.uint8)
     _check(load_library().mglu_unpack_codes_host(_ptr(packed), n_m, h, d, w, _ptr(out)), None, "unpack_codes_host")
+    return out
+
+
+def ffn_forward_fused(up: "Mglu", down: "Mglu", x: torch.Tensor, Wt: torch.Tensor, packed: torch.Tensor,
+                      Wo: torch.Tensor, y_mid: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                      stream=None) -> torch.Tensor:
+    """Row f1 fused: out = MGLU(x) Wo^T in one launch (mglu_ffn_forward).  `up` is the MGLU handle
+    (d, h, n_m), `down` a dense handle (h, d_out, 0); y_mid [B][h] receives MGLU(x) (bf16)."""
+    up._check_inputs(x, Wt, packed)
+    B = x.shape[0]
+    if Wo.dtype != torch.bfloat16 or tuple(Wo.shape) != (down.h, up.h) or not Wo.is_contiguous() or Wo.device != x.device:
+        raise MgluError(MGLU_ERR_INVALID_ARG, "Wo must be a contiguous bf16 [d_out][h] tensor on x's device")
+    if y_mid is None:
+        y_mid = torch.empty((B, up.h), dtype=torch.bfloat16, device=x.device)
+    if out is None:
+        out = torch.empty((B, down.h), dtype=torch.bfloat16, device=x.device)
+    for t, shape in ((y_mid, (B, up.h)), (out, (B, down.h))):
+        if t.dtype != torch.bfloat16 or tuple(t.shape) != shape or not t.is_contiguous() or t.device != x.device:
+            raise MgluError(MGLU_ERR_INVALID_ARG, f"y_mid / out must be contiguous bf16 {shape} tensors on x's device")
+    _check(load_library().mglu_ffn_forward(up.handle, down.handle, _ptr(x), B, _ptr(Wt), _ptr(packed), _ptr(Wo),
+                                           _ptr(y_mid), _ptr(out), _stream_ptr(stream, x.device)), up.handle,
+           "mglu_ffn_forward")
     return out
 
 
