@@ -1,6 +1,4 @@
-# baseline: the driver's exact bench command x3, then a 500-step run
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
-for r in 1 2 3; do python bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu-baseline --no-comparator > gpurun_out/base_d20_$r.json 2> gpurun_out/base_d20_$r.err; done
-python bench.py --steps 500 --no-cpu-baseline --no-comparator > gpurun_out/base_500.json 2> gpurun_out/base_500.err
-for f in gpurun_out/base_*.json; do python -c "import json,sys; d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(d['us_per_call'],2), 'us', round(d['roofline']['frac'],3), d['e2e']['us_per_call'], d['clocks'])"; done
+# baseline check: GPU suite + driver-style default bench (20 steps) + batch sweep of the bf16 paths
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/base_tests.log 2>&1; tail -2 gpurun_out/base_tests.log
+timeout 300 python bench.py --steps 20 --warmup 5 > gpurun_out/base_bench.json 2> gpurun_out/base_bench.err; tail -c 600 gpurun_out/base_bench.json
