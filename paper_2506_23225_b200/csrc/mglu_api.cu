@@ -12,7 +12,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 #include <string>
 #include <type_traits>
 
@@ -54,6 +56,17 @@ struct mglu_ctx {
   };
   std::array<DecMaps, 16> dec_cache;
   uint64_t dec_clock = 0;
+  // W / code descriptors of the tcgen05 paths, keyed by (kind, Wt, codes, box shape): only x's
+  // descriptor is encoded per call
+  struct TcMaps {
+    bool valid = false;
+    int kind = 0, a = 0, b = 0;
+    const void* Wt = nullptr;
+    const void* codes = nullptr;
+    uint64_t stamp = 0;
+    CUtensorMap m[4];
+  };
+  std::array<TcMaps, 16> tc_cache;
   // stream-K decode (tcgen05) workspace: published partials + one ticket per 128-row tile (0
   // between calls: a tile's last arriver re-arms it), allocated / grown on first use
   float* sk_ws = nullptr;
@@ -103,6 +116,20 @@ mglu_status set_err(mglu_ctx* hd, mglu_status s, const std::string& msg) {
     hd->err = msg;
   }
   return s;
+}
+
+// the opt-in dynamic shared-memory limit is a per-kernel (per-device) attribute: raise it to the
+// device maximum once per kernel instead of on every launch
+cudaError_t smem_optin(const void* kern, int device, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_pair(kern, device);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[key] = bytes;
+  return e;
 }
 
 // launch with programmatic stream serialisation (PDL): the kernels call griddepcontrol.wait
@@ -257,6 +284,30 @@ bool dec_maps(mglu_ctx* hd, const void* Wt, const void* codes, mglu::DecMaps* ou
   return true;
 }
 
+// cached W / code descriptors of a tcgen05 path (see mglu_ctx::tc_cache); `build` encodes m[0..3]
+template <typename Build>
+bool tc_maps(mglu_ctx* hd, int kind, const void* Wt, const void* codes, int a, int b, CUtensorMap* out, Build build) {
+  std::lock_guard<std::mutex> g(hd->mu);
+  for (auto& e : hd->tc_cache)
+    if (e.valid && e.kind == kind && e.Wt == Wt && e.codes == codes && e.a == a && e.b == b) {
+      e.stamp = ++hd->dec_clock;
+      std::memcpy(out, e.m, sizeof(e.m));
+      return true;
+    }
+  CUtensorMap m[4];
+  if (!build(m)) return false;
+  size_t victim = 0;
+  for (size_t i = 0; i < hd->tc_cache.size(); ++i) {
+    if (!hd->tc_cache[i].valid) { victim = i; break; }
+    if (hd->tc_cache[i].stamp < hd->tc_cache[victim].stamp) victim = i;
+  }
+  auto& e = hd->tc_cache[victim];
+  e.valid = true; e.kind = kind; e.Wt = Wt; e.codes = codes; e.a = a; e.b = b; e.stamp = ++hd->dec_clock;
+  std::memcpy(e.m, m, sizeof(m));
+  std::memcpy(out, m, sizeof(m));
+  return true;
+}
+
 // shared-memory budget of the HMMA decode kernel in KB (sets the ring depth; MGLU_DEC_SMEM_KB
 // overrides, for experiments)
 int dec_smem_kb() {
@@ -345,7 +396,7 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   }
   const size_t smem = (size_t)p.stages * SB + 2 * p.stages * sizeof(uint64_t) + partbytes + xbytes;
   auto kern = mglu::gemv_mma_kernel<NM, ACT, NB, KSEL, PL>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin((const void*)kern, hd->device, std::max((int)smem, hd->max_smem_optin));
   if (e != cudaSuccess) return e;
   return launch_pdl(kern, dim3((unsigned)ncta), dim3(mglu::kDecThreads), smem, cl.st, p, maps);
 }
@@ -458,7 +509,7 @@ cudaError_t run_ffn(mglu_ctx* up, mglu_ctx* down, const void* x, int B, const vo
   p1.stages = p2.stages = S;
   const size_t smem = (size_t)S * SB + 2 * S * sizeof(uint64_t) + partbytes + xbytes;
   auto kern = mglu::ffn_mma_kernel<NM, ACT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin((const void*)kern, up->device, std::max((int)smem, up->max_smem_optin));
   if (e != cudaSuccess) return e;
   if (!up->ffn_bar) {
     if ((e = cudaMalloc(&up->ffn_bar, 2 * sizeof(unsigned))) != cudaSuccess) return e;
@@ -551,11 +602,19 @@ cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
                       const Call& cl) {
   CUtensorMap mX, mW, mC;
   const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
+  CUtensorMap m[4];
   if (!encode_2d_bf16(&mX, x, hd->d, B, mglu::kTcK, BN, sw) ||
-      !encode_2d_bf16(&mW, Wt, hd->d, hd->h, mglu::kTcK, 128, sw) ||
-      !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, mglu::tc_code_words<NM>(), 128,
-                     code_swizzle(mglu::tc_code_words<NM>() * 4)))
+      !tc_maps(hd, 3, Wt, codes, mglu::tc_code_words<NM>(), 0, m, [&](CUtensorMap* o) {
+        const bool ok = encode_2d_bf16(&o[0], Wt, hd->d, hd->h, mglu::kTcK, 128, sw) &&
+                        encode_2d_u32(&o[1], codes, (uint64_t)hd->d / 32 * NM, hd->h, mglu::tc_code_words<NM>(), 128,
+                                      code_swizzle(mglu::tc_code_words<NM>() * 4));
+        o[2] = o[0];
+        o[3] = o[1];
+        return ok;
+      }))
     return cudaErrorInvalidValue;
+  mW = m[0];
+  mC = m[1];
   mglu::TcParams p;
   p.out = (__nv_bfloat16*)out;
   p.G = cl.G;
@@ -573,7 +632,7 @@ cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   p.stages = S;
   const size_t smem = (size_t)S * SB + fixed;
   auto kern = mglu::gemm_tc_kernel<NM, ACT, BN>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin((const void*)kern, hd->device, std::max((int)smem, hd->max_smem_optin));
   if (e != cudaSuccess) return e;
   constexpr int NSPLIT = mglu::tc_split<NM>();
   const dim3 grid((unsigned)((B + BN - 1) / BN), (unsigned)((hd->h + 127) / 128), NSPLIT);
@@ -721,20 +780,29 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
     p.tr_rem = (int)(hd->h % nt);
     const uint32_t rb = (uint32_t)p.tr_base + (p.tr_rem ? 1u : 0u);
     const uint64_t crow = (uint64_t)hd->d / 32 * NM;
-    if (!encode_2d_bf16(&mW, Wt, hd->d, hd->h, 64, rb, sw) ||
-        !encode_2d_u32(&mC, codes, crow, hd->h, C::CWORDS, rb, code_swizzle(C::CWORDS * 4)) ||
-        !encode_2d_bf16(&mWb, Wt, hd->d, hd->h, 64, (uint32_t)p.tr_base, sw) ||
-        !encode_2d_u32(&mCb, codes, crow, hd->h, C::CWORDS, (uint32_t)p.tr_base, code_swizzle(C::CWORDS * 4)))
+    CUtensorMap m[4];
+    if (!tc_maps(hd, 1, Wt, codes, (int)rb, p.tr_base * 64 + C::CWORDS, m, [&](CUtensorMap* o) {
+          return encode_2d_bf16(&o[0], Wt, hd->d, hd->h, 64, rb, sw) &&
+                 encode_2d_u32(&o[1], codes, crow, hd->h, C::CWORDS, rb, code_swizzle(C::CWORDS * 4)) &&
+                 encode_2d_bf16(&o[2], Wt, hd->d, hd->h, 64, (uint32_t)p.tr_base, sw) &&
+                 encode_2d_u32(&o[3], codes, crow, hd->h, C::CWORDS, (uint32_t)p.tr_base, code_swizzle(C::CWORDS * 4));
+        }))
       return cudaErrorInvalidValue;
+    mW = m[0]; mC = m[1]; mWb = m[2]; mCb = m[3];
     p.units_base = p.units_rem = 0;
     p.ws = nullptr;
     p.tickets = nullptr;
   } else {
-    if (!encode_3d_blocks(&mW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, 128, KB, sw) ||
-        !encode_2d_u32(&mC, codes, (uint64_t)hd->d / 32 * NM, hd->h, C::CWORDS, 128, code_swizzle(C::CWORDS * 4)))
+    CUtensorMap m[4];
+    if (!tc_maps(hd, 2, Wt, codes, C::CWORDS, 0, m, [&](CUtensorMap* o) {
+          const bool ok = encode_3d_blocks(&o[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wt, hd->d, hd->h, 64, 128, KB, sw) &&
+                          encode_2d_u32(&o[1], codes, (uint64_t)hd->d / 32 * NM, hd->h, C::CWORDS, 128, code_swizzle(C::CWORDS * 4));
+          o[2] = o[0];
+          o[3] = o[1];
+          return ok;
+        }))
       return cudaErrorInvalidValue;
-    mWb = mW;
-    mCb = mC;
+    mW = m[0]; mC = m[1]; mWb = m[2]; mCb = m[3];
     const int64_t units = (hd->h + 127) / 128 * p.upt;
     G = std::min<int64_t>(hd->num_sms, units);
     p.units_base = (int)(units / G);
@@ -764,15 +832,8 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   p.wstages = (int)std::min<size_t>(sk_max_wstages(), (cap - fixed) / p.wsb);
   const size_t smem = (size_t)p.wstages * p.wsb + fixed;
   auto kern = one_seg ? mglu::gemv_tc_kernel<NM, BN, MG, true> : mglu::gemv_tc_kernel<NM, BN, MG, false>;
-  // the opt-in shared-memory limit is a per-kernel attribute: set it once (the maximum), not per launch
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(mglu::gemv_tc_kernel<NM, BN, MG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(mglu::gemv_tc_kernel<NM, BN, MG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
+  cudaError_t e = smem_optin((const void*)kern, hd->device, hd->max_smem_optin);
+  if (e != cudaSuccess) return e;
   return launch_pdl(kern, dim3((unsigned)G), dim3(C::THREADS), smem, cl.st, p, mW, mX, mC, mWb, mCb);
 }
 
