@@ -10,7 +10,7 @@ from synth import make_inputs
 
 ACTS = {"identity": 0, "swish": 1, "gelu": 2, "relu": 3, "sigmoid": 4}
 TOL = {"bf16": 1e-2, "f32": 1e-5}          # north_star: max relative error, normwise (R10)
-TIGHT = {"bf16": 5e-3, "f32": 1e-6}        # regression band: a correct kernel lands well inside
+TIGHT = {"bf16": 4e-3, "f32": 1e-6}        # regression band (a correct bf16 kernel lands at 1.8-2.3e-3)
 
 
 def normwise_err(y: np.ndarray, ref: np.ndarray) -> float:
