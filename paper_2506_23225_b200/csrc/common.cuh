@@ -40,38 +40,61 @@ __device__ __forceinline__ float act_rt(int act, float z) {
   }
 }
 
+// g for the bf16 tensor-core epilogues (tile GEMM, tcgen05 GEMV), which evaluate it for every
+// (token, row, mask): Swish and sigmoid by ex2.approx + rcp.approx (__expf / __fdividef; relative
+// error ~1e-6, far below the 2^-9 of the bf16 output) instead of expf + an IEEE division -- the
+// accurate form cost 16 % of the prefill (profiles/r02/prefill_epilogue.txt).  The fp32 SIMT path
+// and the HMMA decode kernel (a few outputs per thread) keep act_g.
+template <int ACT>
+__device__ __forceinline__ float act_fast(float z, int act = 0);
+__device__ __forceinline__ float act_rt_fast(int act, float z) {
+  switch (act) {
+    case kSwish: return act_fast<kSwish>(z);
+    case kSigmoid: return act_fast<kSigmoid>(z);
+    default: return act_rt(act, z);
+  }
+}
+template <int ACT>
+__device__ __forceinline__ float act_fast(float z, int act) {
+  if constexpr (ACT == kRuntimeAct) return act_rt_fast(act, z);
+  else if constexpr (ACT == kSwish) return __fdividef(z, 1.0f + __expf(-z));
+  else if constexpr (ACT == kSigmoid) return __fdividef(1.0f, 1.0f + __expf(-z));
+  else return act_g<ACT>(z);
+}
+
 // Eq. 3 epilogue for one output: y = sum_i g(s_i) * (t - s_i)  (value = t - s_i)
-template <int ACT, int NM>
+// (FAST: act_fast, for the bf16 kernels; the fp32 SIMT path keeps act_g)
+template <int ACT, int NM, bool FAST = false>
 __device__ __forceinline__ float mglu_epilogue(float t, const float (&s)[NM], int act = 0) {
   float y = 0.0f;
 #pragma unroll
-  for (int i = 0; i < NM; ++i) y = fmaf(act_g<ACT>(s[i], act), t - s[i], y);
+  for (int i = 0; i < NM; ++i) y = fmaf((FAST ? act_fast<ACT>(s[i], act) : act_g<ACT>(s[i], act)), t - s[i], y);
   return y;
 }
 
 // Top-K routed epilogue (Appendix B): y = sum_i G_i g(s_i) (t - s_i); gw == nullptr is
 // the plain Eq. 3 (every G_i = 1)
-template <int ACT, int NM>
+template <int ACT, int NM, bool FAST = false>
 __device__ __forceinline__ float mglu_epilogue_w(float t, const float (&s)[NM], const float* gw, int act = 0) {
-  if (!gw) return mglu_epilogue<ACT, NM>(t, s, act);
+  if (!gw) return mglu_epilogue<ACT, NM, FAST>(t, s, act);
   float y = 0.0f;
 #pragma unroll
-  for (int i = 0; i < NM; ++i) y = fmaf(gw[i] * act_g<ACT>(s[i], act), t - s[i], y);
+  for (int i = 0; i < NM; ++i) y = fmaf(gw[i] * (FAST ? act_fast<ACT>(s[i], act) : act_g<ACT>(s[i], act)), t - s[i], y);
   return y;
 }
 
 // Partial-mask ablation variants (reading R20: per mask term): 1 NG gate = t,
 // 2 NV value = t, 3 NM both; 0 = Eq. 3.  Optional routed weights gw.
-template <int ACT, int NM>
+template <int ACT, int NM, bool FAST = false>
 __device__ __forceinline__ float mglu_epilogue_v(float t, const float (&s)[NM], const float* gw, int variant,
                                                  int act = 0) {
-  if (variant == 0) return mglu_epilogue_w<ACT, NM>(t, s, gw, act);
+  if (variant == 0) return mglu_epilogue_w<ACT, NM, FAST>(t, s, gw, act);
   float y = 0.0f;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
     const float gate = (variant & 1) ? t : s[i];
     const float value = (variant & 2) ? t : t - s[i];
-    y = fmaf((gw ? gw[i] : 1.0f) * act_g<ACT>(gate, act), value, y);
+    y = fmaf((gw ? gw[i] : 1.0f) * (FAST ? act_fast<ACT>(gate, act) : act_g<ACT>(gate, act)), value, y);
   }
   return y;
 }

@@ -315,7 +315,11 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
           const float gate = (p.variant & 1) ? t : sg;                    // ablation variants
           const float value = (p.variant & 2) ? t : t - sg;
           const float wgt = p.G ? (tq < p.B ? p.G[(size_t)tq * NM + moff + i] : 0.f) : 1.f;   // routed (App. B)
-          acc = fmaf(wgt * act_g<ACT>(gate, p.act), value, acc);                 // g(s_i) (t - s_i)
+#ifdef MGLU_TC_EPI_ABL   // timing ablation (wrong results): no activation in the epilogue
+          acc = fmaf(wgt * gate, value, acc);
+#else
+          acc = fmaf(wgt * act_fast<ACT>(gate, p.act), value, acc);              // g(s_i) (t - s_i)
+#endif
         }
         yp[ch][q] = acc;
       }

@@ -497,9 +497,9 @@ __device__ __forceinline__ void dec_consume(const DecParams& p, uint8_t* ring, u
             const float* gw = p.G + (size_t)tok * NM;
 #pragma unroll
             for (int k = 0; k < KSEL; ++k)
-              if ((valid >> k) & 1u) y = fmaf(gw[sel[k]] * act_g<ACT>(sv[k], p.act), v[nb][0] - sv[k], y);
+              if ((valid >> k) & 1u) y = fmaf(gw[sel[k]] * act_fast<ACT>(sv[k], p.act), v[nb][0] - sv[k], y);
           } else {
-            y = mglu_epilogue_v<ACT, NM>(v[nb][0], sv, p.G ? p.G + (size_t)tok * NM : nullptr, p.variant, p.act);   // Eq. 3 / routed / variant
+            y = mglu_epilogue_v<ACT, NM, true>(v[nb][0], sv, p.G ? p.G + (size_t)tok * NM : nullptr, p.variant, p.act);   // Eq. 3 / routed / variant
           }
           p.out[(size_t)tok * p.h + r0 + row] = __float2bfloat16_rn(y);
         }

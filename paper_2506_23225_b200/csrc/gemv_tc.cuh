@@ -137,8 +137,8 @@ __device__ __forceinline__ void sk_ld_chunk(uint32_t abase, int ch, float (&f)[N
 
 // Eq. 3 epilogue (a6, a7) of token chunk ch of tile row `grow` from its summed accumulators f[0] = t,
 // f[1 + i] = u_i (s_i = (t + u_i) / 2), or Alg. 1's z when p.z is set
-template <int NM, int CH>
-__device__ __forceinline__ void sk_epi_store(const SkParams& p, const float (&f)[NM + 1][CH], int ch, int grow) {
+template <int NM, int CH, int ACT>
+__device__ __forceinline__ void sk_epi_store_g(const SkParams& p, const float (&f)[NM + 1][CH], int ch, int grow) {
 #pragma unroll
   for (int q = 0; q < CH; ++q) {
     const int tok = ch * CH + q;
@@ -161,10 +161,16 @@ __device__ __forceinline__ void sk_epi_store(const SkParams& p, const float (&f)
       const float gate = (p.variant & 1) ? t : sg;              // ablation variants
       const float value = (p.variant & 2) ? t : t - sg;
       const float wgt = p.G ? p.G[(size_t)tok * NM + i] : 1.f;  // routed (Appendix B)
-      y = fmaf(wgt * act_rt(p.act, gate), value, y);
+      y = fmaf(wgt * act_fast<ACT>(gate, p.act), value, y);
     }
     p.out[(size_t)tok * p.h + grow] = __float2bfloat16_rn(y);
   }
+}
+// g resolved once per chunk, not per output: Swish (the default) inline, the others through act_rt
+template <int NM, int CH>
+__device__ __forceinline__ void sk_epi_store(const SkParams& p, const float (&f)[NM + 1][CH], int ch, int grow) {
+  if (p.act == kSwish) sk_epi_store_g<NM, CH, kSwish>(p, f, ch, grow);
+  else sk_epi_store_g<NM, CH, kRuntimeAct>(p, f, ch, grow);
 }
 
 // ONE: the CTA has a single segment (row split, one tile per CTA): one accumulator set and the TMEM
