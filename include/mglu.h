@@ -89,7 +89,7 @@ typedef enum {
 
 typedef enum { MGLU_BF16 = 0, MGLU_F32 = 1 } mglu_dtype;
 
-/* Kernel regime.  AUTO picks by dtype and B (bf16 B <= 4 MMA, 5..48 TCROW on layers
+/* Kernel regime.  AUTO picks by dtype and B (bf16 B <= 4 MMA, 5..32 TCROW on layers
  * with >= 64 rows per SM (else TCDEC up to 16), larger TCGEN05; n_m = 16 TCGEN05; fp32 SIMT; a path
  * that refuses the shape falls through).  The others force one
  * kernel (for tests and benchmarks); forcing a path that cannot serve the configuration makes

@@ -693,7 +693,7 @@ cudaError_t tc_nm(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const 
 
 // ------------------------------------------------------------------ tcgen05 stream-K decode dispatch
 constexpr int kSkMaxB = 64;
-constexpr int kAutoMmaMaxB = 4, kAutoSkMaxB = 16, kAutoRowMaxB = 48;
+constexpr int kAutoMmaMaxB = 4, kAutoSkMaxB = 16, kAutoRowMaxB = 32;
 
 bool sk_can_serve(const mglu_ctx* hd, int64_t B) {
   // 128-column units; mask-word rows of d/32 * n_m u32 words must be 16-byte multiples (TMA)
@@ -1021,7 +1021,7 @@ static int auto_path(const mglu_ctx* hd, int64_t B) {
   int path;
   // measured crossovers at the Llama-3-8B FFN shape (profiles/r02/tcrow_sweep.txt): the
   // register-masked HMMA kernel for B <= 4 (one 8-column MMA tile), the tcgen05 GEMV for
-  // 5 <= B <= 48 on wide layers as its row split (stream-K up to 16 on narrow ones),
+  // 5 <= B <= 32 on wide layers as its row split (stream-K up to 16 on narrow ones),
   // the tcgen05 tile GEMM above; SIMT for fp32 and shapes the others refuse
   // (n_m = 8 on large layers: the HMMA kernel's 9 MMAs per step make it compute-bound, and the
   //  stream-K tcgen05 GEMV wins from B = 1: 129 vs 138 us at d=8192 h=28672; on small shards

@@ -111,7 +111,7 @@ def test_full_size_tensor_core_sampled(name, d, h, n_m, B):
     y = layer.forward(x, Wt, packed)
     torch.cuda.synchronize()
     wide = h >= torch.cuda.get_device_properties(0).multi_processor_count * 64
-    want = "tcrow" if (5 <= B <= 48 and n_m <= 4 and wide) else ("tcdec" if B <= 16 else "tcgen05")
+    want = "tcrow" if (5 <= B <= 32 and n_m <= 4 and wide) else ("tcdec" if B <= 16 else "tcgen05")
     assert layer.last_path() == want                               # AUTO crossovers
     rng = np.random.default_rng(B + n_m)
     toks = np.unique(np.concatenate([[0, B - 1], rng.choice(B, min(B, 46), replace=False)]))

@@ -1,7 +1,7 @@
 """Column-shard parity on one GPU: G handles Mglu(d, h/G) each run on their row
 slice (pointer offsets into Wt and the packed codes, paper_2506_23225_b200.shard) and the
 concatenated outputs equal the unsharded layer (P8) -- bit-identically on the tcgen05 tile
-GEMM and on the row-split tcgen05 GEMV (MGLU_PATH_TCROW, AUTO for 5 <= B <= 48): on both a row's
+GEMM and on the row-split tcgen05 GEMV (MGLU_PATH_TCROW, AUTO for 5 <= B <= 32): on both a row's
 k-order is unit by unit, k16 step by k16 step, whatever tile or CTA holds it.  The HMMA decode
 kernel (AUTO for B <= 4) re-splits a stage's columns over 2..16 warps by the CTA's row count for
 throughput, so its shards are held to the bf16 bound against the oracle instead (R21)."""
