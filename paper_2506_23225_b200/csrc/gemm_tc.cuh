@@ -274,6 +274,10 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
     pdl_wait();                                            // out may be read upstream
     const uint32_t lane_base = tmem + lane_off;
     static_assert(HALF % 8 == 0, "BN / 2 must be a multiple of 8");
+#ifdef MGLU_TC_EPI_SKIP   // timing ablation (wrong results): no epilogue at all
+    if (true) {
+    } else
+#endif
     if (p.z) {
       // partials (debug / parity of a5, a6): this CTA's masks' s_i and t - s_i, no reduction.  A
       // separate loop: a partials branch inside the y loop below cost the BN = 64 tile 2x (measured)

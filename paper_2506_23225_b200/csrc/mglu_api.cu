@@ -735,7 +735,7 @@ int sk_rows_env() {
 int sk_max_wstages() {
   static const int v = [] {
     const char* e = getenv("MGLU_SK_WSTAGES");   // experiments: W ring depth cap
-    return e ? atoi(e) : 5;   // 5: measured (row split at B = 16: 35.0 us vs 35.7 with 6)
+    return e ? atoi(e) : 3;   // 3: measured best after the epilogue fix (row split B = 8: 29.7 us vs 30.7 with 5, 31.3 with 6; profiles/r02/tc_gemv_experiments.txt)
   }();
   return v;
 }
