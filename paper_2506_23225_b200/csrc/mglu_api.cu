@@ -597,6 +597,14 @@ bool encode_2d_u32(CUtensorMap* m, const void* base, uint64_t cols, uint64_t row
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+int tc_max_stages() {
+  static const int v = [] {
+    const char* e = getenv("MGLU_TC_STAGES");   // experiments: ring depth cap of the tile GEMM
+    return e ? std::max(2, atoi(e)) : 8;
+  }();
+  return v;
+}
+
 template <int NM, int ACT, int BN>
 cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, const void* codes, void* out,
                       const Call& cl) {
@@ -628,7 +636,7 @@ cudaError_t run_tc_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   const size_t fixed = 1024 + 256 + mglu::tc_red_bytes<NM, BN>();   // alignment slack + barriers + split buffer
   const size_t cap = (size_t)hd->max_smem_optin;
   if (cap < fixed + 2 * SB) return cudaErrorInvalidConfiguration;
-  const int S = (int)std::min<size_t>(8, (cap - fixed) / SB);
+  const int S = (int)std::min<size_t>((size_t)tc_max_stages(), (cap - fixed) / SB);
   p.stages = S;
   const size_t smem = (size_t)S * SB + fixed;
   auto kern = mglu::gemm_tc_kernel<NM, ACT, BN>;
