@@ -335,7 +335,13 @@ gemm_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap mX, const _
         }
       } else {
         const int grow = m0 + m;
+#ifdef MGLU_TC_EPI_NOSTORE   // timing ablation (wrong results): the epilogue without its global stores
+        if (grow < 0) {
+#elif defined(MGLU_TC_EPI_MATHONLY)   // timing ablation: the math kept (consumed), stores almost never
+        if (yp[ch][0] + yp[ch][1] + yp[ch][2] + yp[ch][3] + yp[ch][4] + yp[ch][5] + yp[ch][6] + yp[ch][7] == 1234.5f) {
+#else
         if (grow < p.h) {
+#endif
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int tok = n0 + c0 + q;
