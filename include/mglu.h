@@ -171,7 +171,8 @@ mglu_status mglu_forward_routed(mglu_handle hd, const void* x, int64_t B, const 
  * with a grid-wide barrier (cooperative launch: all CTAs resident, one per SM) between the phases;
  * the result equals up.forward followed by down.forward bit for bit.  bf16, 1 <= B <= 4,
  * d % 128 == 0 and h % 128 == 0, Swish at n_m = 8, else UNSUPPORTED; mismatched handles INVALID_ARG.  The up
- * handle keeps the barrier state (8 bytes, allocated on the first call). */
+ * handle keeps the barrier state (8 bytes, allocated on the first call): one stream at a time per
+ * up handle.  x, y_mid and out must be distinct buffers (INVALID_ARG otherwise). */
 mglu_status mglu_ffn_forward(mglu_handle up, mglu_handle down, const void* x, int64_t B, const void* Wt,
                              const void* packed, const void* Wo, void* y_mid, void* out, void* stream);
 

@@ -1186,6 +1186,8 @@ mglu_status mglu_ffn_forward(mglu_handle up, mglu_handle down, const void* x, in
   mglu_status s = check_ptrs(up, x, B, Wt, packed, y_mid);
   if (s != MGLU_OK) return s;
   if (!Wo || !out) return set_err(up, MGLU_ERR_INVALID_ARG, "null W_o / out");
+  if (y_mid == out || y_mid == x || out == x)
+    return set_err(up, MGLU_ERR_INVALID_ARG, "x, y_mid and out must be distinct buffers (phase 2 reads y_mid while writing out)");
   if (!aligned16(Wo) || !aligned16(out)) return set_err(up, MGLU_ERR_MISALIGNED, "W_o / out must be 16-byte aligned");
   if (down->n_m != 0 || down->d != up->h || down->device != up->device || down->dtype != MGLU_BF16)
     return set_err(up, MGLU_ERR_INVALID_ARG, "down must be a dense (n_m = 0) bf16 handle with d = up.h on up's device");

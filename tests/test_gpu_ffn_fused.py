@@ -101,7 +101,7 @@ def test_fused_ffn_other_activation_and_output_width():
     assert normwise_err(out.float().cpu().numpy().astype(np.float64), ref) <= TIGHT["bf16"]
 
 
-@pytest.mark.parametrize("case", ["B5", "nm8_gelu", "mismatch"])
+@pytest.mark.parametrize("case", ["B5", "nm8_gelu", "mismatch", "alias"])
 def test_fused_ffn_refuses(case):
     from paper_2506_23225_b200.mglu import Mglu, MgluError, MGLU_ERR_INVALID_ARG, MGLU_ERR_UNSUPPORTED, ffn_forward_fused
     n_m = 8 if case == "nm8_gelu" else 4
@@ -111,6 +111,12 @@ def test_fused_ffn_refuses(case):
         down = Mglu(2048, 512, 0, dtype="bf16")
         Wo = torch.zeros(512, 1024, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(MgluError) as e:
-        ffn_forward_fused(up, down, x, Wt, packed, Wo)
-    want = MGLU_ERR_INVALID_ARG if case == "mismatch" else MGLU_ERR_UNSUPPORTED
+        if case == "alias":                               # out aliasing y_mid: refused, not corrupted
+            ym = torch.empty(2, 1024, dtype=torch.bfloat16, device="cuda")
+            from paper_2506_23225_b200.mglu import _check, _ptr, _stream_ptr, load_library
+            _check(load_library().mglu_ffn_forward(up.handle, down.handle, _ptr(x), 2, _ptr(Wt), _ptr(packed), _ptr(Wo),
+                                                   _ptr(ym), _ptr(ym), _stream_ptr(None, x.device)), up.handle, "ffn")
+        else:
+            ffn_forward_fused(up, down, x, Wt, packed, Wo)
+    want = MGLU_ERR_INVALID_ARG if case in ("mismatch", "alias") else MGLU_ERR_UNSUPPORTED
     assert e.value.status == want
