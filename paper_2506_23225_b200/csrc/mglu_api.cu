@@ -754,7 +754,10 @@ int sk_max_wstages() {
 bool auto_row_split(const mglu_ctx* hd, int64_t B) {
   const int env = sk_rows_env();
   if (env >= 0) return env == 1;
-  return hd->n_m <= 4 && B >= 5 && hd->h >= (int64_t)hd->num_sms * kSkRowMin;
+  // n_m = 8: only while every CTA has a single tile (h <= 128 #SM; config 3 B = 8: 45.9 vs 51.0 us),
+  // two 97-row tiles per CTA lose to stream-K (config 5 B = 8: 168.6 vs 149.5 us)
+  return B >= 5 && hd->h >= (int64_t)hd->num_sms * kSkRowMin &&
+         (hd->n_m <= 4 || hd->h <= (int64_t)hd->num_sms * 128);
 }
 
 template <int NM, int BN, int MG>
@@ -1034,12 +1037,15 @@ static int auto_path(const mglu_ctx* hd, int64_t B) {
   // (n_m = 8 on large layers: the HMMA kernel's 9 MMAs per step make it compute-bound, and the
   //  stream-K tcgen05 GEMV wins from B = 1: 129 vs 138 us at d=8192 h=28672; on small shards
   //  (h < 8192) the HMMA kernel stays ahead)
-  const bool nm8_big = hd->n_m == 8 && hd->h >= 8192 && sk_can_serve(hd, B);
-  if (B <= kAutoMmaMaxB && mma_can_serve(hd, B) && !nm8_big)
+  // (n_m = 8 on large layers keeps stream-K up to its B <= 32 limit: config 5 B = 32 264.9 vs 275.3 us
+  //  for the tile GEMM; at B <= 4 the HMMA kernel ties or wins: config 5 135.8 vs 136.5, config 3
+  //  38.3 vs 42.8 us -- profiles/r02/nm8_paths.txt)
+  const bool nm8_big = hd->n_m == 8 && hd->h >= 8192;
+  if (B <= kAutoMmaMaxB && mma_can_serve(hd, B))
     path = MGLU_PATH_MMA;
   else if (B <= kAutoRowMaxB && sk_can_serve(hd, B) && auto_row_split(hd, B))
     path = MGLU_PATH_TCROW;
-  else if (B <= kAutoSkMaxB && sk_can_serve(hd, B))
+  else if ((B <= kAutoSkMaxB || nm8_big) && sk_can_serve(hd, B))
     path = MGLU_PATH_TCDEC;
   else if (mma_can_serve(hd, B))
     path = MGLU_PATH_MMA;
