@@ -1037,13 +1037,15 @@ static int auto_path(const mglu_ctx* hd, int64_t B) {
   // (n_m = 8 on large layers: the HMMA kernel's 9 MMAs per step make it compute-bound, and the
   //  stream-K tcgen05 GEMV wins from B = 1: 129 vs 138 us at d=8192 h=28672; on small shards
   //  (h < 8192) the HMMA kernel stays ahead)
-  // (n_m = 8 on large layers keeps stream-K up to its B <= 32 limit: config 5 B = 32 264.9 vs 275.3 us
+  // (the row split's upper batch is 64 / 48 / 32 for n_m = 1 / 2 / >= 4: fewer masked operands per
+  //  unit keep it ahead of the tile GEMM longer -- profiles/r02/nm12_paths.txt;
+  //  n_m = 8 on large layers keeps stream-K up to its B <= 32 limit: config 5 B = 32 264.9 vs 275.3 us
   //  for the tile GEMM; at B <= 4 the HMMA kernel ties or wins: config 5 135.8 vs 136.5, config 3
   //  38.3 vs 42.8 us -- profiles/r02/nm8_paths.txt)
   const bool nm8_big = hd->n_m == 8 && hd->h >= 8192;
   if (B <= kAutoMmaMaxB && mma_can_serve(hd, B))
     path = MGLU_PATH_MMA;
-  else if (B <= kAutoRowMaxB && sk_can_serve(hd, B) && auto_row_split(hd, B))
+  else if (B <= (hd->n_m == 1 ? 64 : hd->n_m == 2 ? 48 : kAutoRowMaxB) && sk_can_serve(hd, B) && auto_row_split(hd, B))
     path = MGLU_PATH_TCROW;
   else if ((B <= kAutoSkMaxB || nm8_big) && sk_can_serve(hd, B))
     path = MGLU_PATH_TCDEC;
