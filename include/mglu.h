@@ -185,7 +185,10 @@ mglu_status mglu_forward_routed_planes(mglu_handle hd, const void* x, int64_t B,
 
 /* End-to-end form: x_host [B][d] and out_host [B][h] are HOST buffers (pinned for async
  * copies; pageable works but serialises).  Copies x to the handle's device staging buffer,
- * runs mglu_forward, copies y back, all enqueued on `stream` (the caller synchronises).  The
+ * runs mglu_forward, copies y back, all enqueued on `stream` (the caller synchronises).  With
+ * page-locked, device-mapped buffers the copies are small kernels chained to the forward by PDL
+ * (its W streaming overlaps x's transfer, the copy-out launches during its tail); other buffers
+ * use cudaMemcpyAsync.  The
  * staging buffer is allocated at the first call for a given B and reused (grown, never shrunk).
  * Errors as mglu_forward plus OOM. */
 mglu_status mglu_forward_host(mglu_handle hd, const void* x_host, int64_t B, const void* Wt,

@@ -1058,6 +1058,38 @@ static int auto_path(const mglu_ctx* hd, int64_t B) {
   return path;
 }
 
+// mglu_forward_host with page-locked, device-mapped host buffers: the copies are small kernels in
+// the PDL chain instead of cudaMemcpyAsync (which the forward kernel could not overlap): the
+// copy-in grid releases its dependent at once, so the forward's producer streams W while x
+// crosses PCIe (the forward reads x only after griddepcontrol.wait); the copy-out grid launches
+// during the forward's tail and waits for it before reading y.
+__global__ void stage_in_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t n) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int64_t n16 = n / 16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (int64_t i = n16 * 16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void stage_out_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t n) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");      // y is the predecessor's output
+  const int64_t n16 = n / 16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (int64_t i = n16 * 16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+// device alias of a page-locked, mapped host buffer (nullptr for pageable / unregistered memory)
+static void* mapped_alias(const void* host) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) { (void)cudaGetLastError(); return nullptr; }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+  return a.devicePointer;
+}
+static unsigned stage_grid(int64_t n) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(64, (n / 16 + 255) / 256));
+}
+
 // test hook: flip one bit of the caller's packed codes (mglu_set_debug)
 __global__ void flip_bit_kernel(uint8_t* p, uint8_t m) { p[0] ^= m; }
 
@@ -1363,13 +1395,23 @@ mglu_status mglu_forward_host(mglu_handle hd, const void* x_host, int64_t B, con
     if (e != cudaSuccess) { hd->y_stage_bytes = 0; if (prev != hd->device) cudaSetDevice(prev); return MGLU_ERR_OOM; }
     hd->y_stage_bytes = yb;
   }
-  e = cudaMemcpyAsync(hd->x_stage, x_host, xb, cudaMemcpyHostToDevice, st);
+  void* xin = mapped_alias(x_host);
+  void* yout = mapped_alias(out_host);
+  if (xin && aligned16(xin))
+    e = launch_pdl(stage_in_kernel, dim3(stage_grid((int64_t)xb)), dim3(256), 0, st, (const uint8_t*)xin,
+                   (uint8_t*)hd->x_stage, (int64_t)xb);
+  else
+    e = cudaMemcpyAsync(hd->x_stage, x_host, xb, cudaMemcpyHostToDevice, st);
   if (prev != hd->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_fail(hd, e, "H2D x");
   mglu_status s = mglu_forward(hd, hd->x_stage, B, Wt, packed, hd->y_stage, stream);
   if (s != MGLU_OK) return s;
   cudaSetDevice(hd->device);
-  e = cudaMemcpyAsync(out_host, hd->y_stage, yb, cudaMemcpyDeviceToHost, st);
+  if (yout && aligned16(yout))
+    e = launch_pdl(stage_out_kernel, dim3(stage_grid((int64_t)yb)), dim3(256), 0, st, (const uint8_t*)hd->y_stage,
+                   (uint8_t*)yout, (int64_t)yb);
+  else
+    e = cudaMemcpyAsync(out_host, hd->y_stage, yb, cudaMemcpyDeviceToHost, st);
   if (prev != hd->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_fail(hd, e, "D2H y");
   return MGLU_OK;

@@ -261,3 +261,31 @@ def test_forward_host_matches_device():
     layer.forward_host(xh, Wt, packed, yh)
     torch.cuda.synchronize()
     assert torch.equal(yh, y.cpu())
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+@pytest.mark.parametrize("B,d,h", [(1, 4096, 14336), (3, 512, 300), (8, 1024, 1000)])
+def test_forward_host_copy_paths(pinned, B, d, h):
+    """mglu_forward_host's two copy paths: page-locked (device-mapped) buffers go through the
+    PDL-chained copy kernels, pageable ones through cudaMemcpyAsync; both give the device result
+    bit for bit, repeated back to back on one stream (the copy-in of call i+1 must not overtake the
+    copy-out of call i)."""
+    from paper_2506_23225_b200.mglu import Mglu
+    from synth import random_packed_codes
+    g = torch.Generator(device="cuda").manual_seed(B + d)
+    x = torch.randn(B, d, device="cuda", generator=g).to(torch.bfloat16)
+    Wt = ((torch.rand(h, d, device="cuda", generator=g) * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+    packed = random_packed_codes(B, h, d, 4, device="cuda")
+    layer = Mglu(d, h, 4, dtype="bf16")
+    xs = [torch.randn(B, d, generator=torch.Generator().manual_seed(k)).to(torch.bfloat16) for k in range(4)]
+    want = [layer.forward(xk.cuda(), Wt, packed).cpu() for xk in xs]
+    if pinned:
+        xs = [xk.pin_memory() for xk in xs]
+    outs = [torch.empty(B, h, dtype=torch.bfloat16) for _ in xs]
+    if pinned:
+        outs = [o.pin_memory() for o in outs]
+    for xk, o in zip(xs, outs):
+        layer.forward_host(xk, Wt, packed, o)
+    torch.cuda.synchronize()
+    for o, w in zip(outs, want):
+        assert torch.equal(o, w)
