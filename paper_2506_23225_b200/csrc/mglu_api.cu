@@ -751,6 +751,13 @@ int sk_max_wstages() {
 // the row split wins once the stream-K fix-up grows with B (from B = 5, tied there) on layers wide enough to give
 // every SM kSkRowMin rows; at n_m = 8 the maskers' cost per 128-row unit dominates and the row
 // split's partly idle lanes lose (config 5, B = 1: 159 vs 129 us)
+int sk_xstages() {
+  static const int v = [] {
+    const char* e = getenv("MGLU_SK_XSTAGES");   // experiments: x ring depth
+    return e ? std::max(2, atoi(e)) : 4;
+  }();
+  return v;
+}
 bool auto_row_split(const mglu_ctx* hd, int64_t B) {
   const int env = sk_rows_env();
   if (env >= 0) return env == 1;
@@ -837,7 +844,7 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
     p.wsb = C::WSB;
   }
   const size_t cap = (size_t)hd->max_smem_optin;
-  p.xstages = 4;
+  p.xstages = sk_xstages();
   const size_t fixed = 1024 + 512 + (size_t)p.xstages * C::XB;   // alignment slack + barriers + x ring
   if (cap < fixed + 2 * (size_t)p.wsb) return cudaErrorInvalidConfiguration;
   p.wstages = (int)std::min<size_t>(sk_max_wstages(), (cap - fixed) / p.wsb);
