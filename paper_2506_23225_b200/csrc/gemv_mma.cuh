@@ -64,7 +64,8 @@ struct DecParams {
   int variant;               // partial-mask ablation variant (0 = Eq. 3; 1 NG, 2 NV, 3 NM)
   int act;                   // g when the kernel is the kRuntimeAct instantiation
   int B, d, h;
-  int tiles_base, tiles_rem; // CTA c owns tiles_base + (c < tiles_rem) 8-row tiles
+  int tiles_base, tiles_rem; // CTA c < ncta owns tiles_base + (c < tiles_rem) 8-row tiles
+  int ncta;                  // CTAs of this pass (the fused FFN grid may be wider: the rest own none)
   int stages;                // ring depth
   int xpar;                  // u32 words per parity array of one token's x in smem (+ pad)
   int l2pf;                  // stages beyond the ring prefetched into L2 once, at the CTA's start
@@ -142,7 +143,7 @@ struct DecGeo {
 __device__ __forceinline__ DecGeo dec_geo(const DecParams& p, int cta) {
   DecGeo g;
   const int tile0 = cta * p.tiles_base + min(cta, p.tiles_rem);
-  const int ntiles = p.tiles_base + (cta < p.tiles_rem ? 1 : 0);
+  const int ntiles = cta < p.ncta ? p.tiles_base + (cta < p.tiles_rem ? 1 : 0) : 0;
   g.r0 = 8 * tile0;
   g.nrows = min(8 * ntiles, p.h - g.r0);
   g.d = p.d;

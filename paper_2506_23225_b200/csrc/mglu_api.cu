@@ -318,6 +318,25 @@ int dec_smem_kb() {
   return v;
 }
 
+// grid of the HMMA decode kernel (experiments: MGLU_DEC_CTAS caps it below the SM count)
+int dec_ctas() {
+  static const int v = [] {
+    const char* e = getenv("MGLU_DEC_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// CTAs of the HMMA decode kernel for this layer: every SM but 4 on large layers -- measured on two
+// boxes at config 3 B = 1: 24.64 vs 24.99 us (the driver's 20-step line 25.24 vs 25.65), config 2
+// within 1 %, config 5 -0.4 % (profiles/r02/dec_grid.txt); MGLU_DEC_CTAS overrides (experiments)
+int64_t dec_grid(const mglu_ctx* hd) {
+  const int64_t tiles = (hd->h + 7) / 8;
+  const int64_t grid = dec_ctas() > 0 ? std::min(dec_ctas(), hd->num_sms)
+                     : (tiles >= (int64_t)hd->num_sms * 8 ? hd->num_sms - 4 : hd->num_sms);
+  return std::max<int64_t>(1, std::min<int64_t>(tiles, grid));
+}
+
 // deeper ring for the CTAs with one tile more (MGLU_DEC_HEAVY=0 disables)
 #ifndef MGLU_DEC_HEAVY_DEFAULT
 #define MGLU_DEC_HEAVY_DEFAULT 1
@@ -369,7 +388,8 @@ cudaError_t run_mma_nb(mglu_ctx* hd, const void* x, int B, const void* Wt, const
   p.h = (int)hd->h;
   // whole 8-row tiles per CTA, one CTA per SM (the last tile of a ragged h is zero-filled by TMA)
   const int64_t tiles = (hd->h + 7) / 8;
-  const int64_t ncta = std::min<int64_t>(tiles, hd->num_sms);
+  const int64_t ncta = dec_grid(hd);
+  p.ncta = (int)ncta;
   p.tiles_base = (int)(tiles / ncta);
   p.tiles_rem = (int)(tiles % ncta);
   p.l2pf = dec_l2pf();
@@ -483,6 +503,7 @@ mglu::DecParams dec_params(const mglu_ctx* hd, const void* x, int B, void* out, 
   p.d = (int)hd->d;
   p.h = (int)hd->h;
   const int64_t tiles = (hd->h + 7) / 8;
+  p.ncta = (int)ncta;
   p.tiles_base = (int)(tiles / ncta);
   p.tiles_rem = (int)(tiles % ncta);
   p.l2pf = 0;
@@ -494,9 +515,11 @@ mglu::DecParams dec_params(const mglu_ctx* hd, const void* x, int B, void* out, 
 template <int NM, int ACT>
 cudaError_t run_ffn(mglu_ctx* up, mglu_ctx* down, const void* x, int B, const void* Wt, const void* codes,
                     const void* Wo, void* ymid, void* out, cudaStream_t st) {
-  const int64_t ncta = std::min<int64_t>((up->h + 7) / 8, up->num_sms);
-  mglu::DecParams p1 = dec_params(up, x, B, ymid, ncta);
-  mglu::DecParams p2 = dec_params(down, ymid, B, out, ncta);
+  // each phase keeps the partition its standalone launch uses (so the result is bit-identical to the
+  // composition); the grid is the wider of the two, the extra CTAs own no tiles in the other phase
+  const int64_t n1 = dec_grid(up), n2 = dec_grid(down), ncta = std::max(n1, n2);
+  mglu::DecParams p1 = dec_params(up, x, B, ymid, n1);
+  mglu::DecParams p2 = dec_params(down, ymid, B, out, n2);
   mglu::DecMaps m1, m2;
   if (!dec_maps(up, Wt, codes, &m1) || !dec_maps(down, Wo, nullptr, &m2)) return cudaErrorInvalidValue;
   constexpr size_t SB = mglu::dec_stage_bytes<NM>();
