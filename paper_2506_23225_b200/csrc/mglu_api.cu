@@ -774,6 +774,13 @@ int sk_max_wstages() {
 // the row split wins once the stream-K fix-up grows with B (from B = 5, tied there) on layers wide enough to give
 // every SM kSkRowMin rows; at n_m = 8 the maskers' cost per 128-row unit dominates and the row
 // split's partly idle lanes lose (config 5, B = 1: 159 vs 129 us)
+int sk_ctas() {
+  static const int v = [] {
+    const char* e = getenv("MGLU_SK_CTAS");   // experiments: row-split grid
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
 int sk_xstages() {
   static const int v = [] {
     const char* e = getenv("MGLU_SK_XSTAGES");   // experiments: x ring depth
@@ -814,7 +821,9 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
   if (p.row_mode) {
     // G CTAs x tpc tiles of tr_base or tr_base + 1 (<= 128) rows; the first tr_rem tiles are the big
     // ones.  Boxes of exactly a tile's rows: nothing is read twice or past the tile.
-    G = std::min<int64_t>(hd->num_sms, hd->h);
+    // every SM but 4, as the HMMA kernel (config 3 B = 8 / 16 / 32: 29.41 / 30.14 / 35.15 us vs
+    // 29.78 / 30.55 / 36.10 on all 148; profiles/r02/dec_grid.txt)
+    G = std::min<int64_t>(sk_ctas() > 0 ? std::min(sk_ctas(), hd->num_sms) : std::max(1, hd->num_sms - 4), hd->h);
     p.tpc = (int)((hd->h + G * 128 - 1) / (G * 128));
     const int64_t nt = G * p.tpc;
     p.tr_base = (int)(hd->h / nt);
