@@ -854,7 +854,7 @@ cudaError_t run_sk_bn(mglu_ctx* hd, const void* x, int64_t B, const void* Wt, co
       return cudaErrorInvalidValue;
     mW = m[0]; mC = m[1]; mWb = m[2]; mCb = m[3];
     const int64_t units = (hd->h + 127) / 128 * p.upt;
-    G = std::min<int64_t>(hd->num_sms, units);
+    G = std::min<int64_t>(sk_ctas() > 0 ? std::min(sk_ctas(), hd->num_sms) : hd->num_sms, units);
     p.units_base = (int)(units / G);
     p.units_rem = (int)(units % G);
     p.tpc = p.tr_base = p.tr_rem = 0;
