@@ -793,8 +793,12 @@ bool auto_row_split(const mglu_ctx* hd, int64_t B) {
   if (env >= 0) return env == 1;
   // n_m = 8: only while every CTA has a single tile (h <= 128 #SM; config 3 B = 8: 45.9 vs 51.0 us),
   // two 97-row tiles per CTA lose to stream-K (config 5 B = 8: 168.6 vs 149.5 us)
-  return B >= 5 && hd->h >= (int64_t)hd->num_sms * kSkRowMin &&
-         (hd->n_m <= 4 || hd->h <= (int64_t)hd->num_sms * 128);
+  if (B < 5) return false;
+  if (hd->h >= (int64_t)hd->num_sms * kSkRowMin) return hd->n_m <= 4 || hd->h <= (int64_t)hd->num_sms * 128;
+  // narrow layers (h-shards): the row split costs ~29 us whatever the rows (every CTA walks all of d),
+  // which beats the stream-K fix-up from B = 16 and the tile GEMM up to B = 32 (h = 1792 / 3584 /
+  // 7168, B = 16: 29.4 / 29.5 / 29.7 us vs stream-K 45.1 / 30.6 / 29.4; profiles/r02/narrow_paths.txt)
+  return hd->n_m <= 4 && B >= 16;
 }
 
 template <int NM, int BN, int MG>
