@@ -89,9 +89,11 @@ typedef enum {
 
 typedef enum { MGLU_BF16 = 0, MGLU_F32 = 1 } mglu_dtype;
 
-/* Kernel regime.  AUTO picks by dtype and B (bf16 B <= 4 MMA, 5..32 TCROW on layers
- * with >= 64 rows per SM (else TCDEC up to 16), larger TCGEN05; n_m = 16 TCGEN05; fp32 SIMT; a path
- * that refuses the shape falls through).  The others force one
+/* Kernel regime.  AUTO picks by dtype, n_m, h and B from measured crossovers: bf16
+ * B <= 4 MMA; 5..32 TCROW on layers with >= 64 rows per SM (to 48 / 64 at n_m = 2 / 1; at n_m = 8
+ * only with one tile per CTA), on narrower layers TCDEC up to 15 and TCROW 16..32; n_m = 8 on
+ * large layers TCDEC up to 32; larger B TCGEN05; n_m = 16 TCGEN05; fp32 SIMT; a path that refuses
+ * the shape falls through.  The others force one
  * kernel (for tests and benchmarks); forcing a path that cannot serve the configuration makes
  * mglu_forward return MGLU_ERR_UNSUPPORTED. */
 typedef enum {
